@@ -1,0 +1,551 @@
+// Tape -> SSA program -> sm_100a CUDA source.  See codegen.h.
+#include "codegen.h"
+
+#include <algorithm>
+#include <cinttypes>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <queue>
+#include <unordered_map>
+
+namespace vsb {
+
+// operand counts, symcore.py:100-124
+static const int kArity[OP_COUNT] = {0, 0, 1, 1, 2, 2, 2, 2, 1, 1, 1, 2, 1, 1, 1, 1, 1, 2, 1, 2, 2, 1, 3};
+
+int op_arity(int op) { return (op >= 0 && op < OP_COUNT) ? kArity[op] : -1; }
+
+static std::string row_err(int64_t i, const std::string& msg) {
+    return "instruction " + std::to_string(i) + ": " + msg;
+}
+
+std::string build_program(const int32_t* code, const double* values, int64_t n_rows, int64_t n_w,
+                          const int64_t* nnz_in, int32_t n_in, const int64_t* nnz_out, int32_t n_out,
+                          Program* out) {
+    if (n_rows < 0 || n_w < 0 || n_in < 0 || n_out < 0) return "negative tape dimension";
+    Program p;
+    p.n_rows = n_rows;
+    p.n_w = n_w;
+    p.nnz_in.assign(nnz_in, nnz_in + n_in);
+    p.nnz_out.assign(nnz_out, nnz_out + n_out);
+    for (auto v : p.nnz_in) if (v < 0) return "negative input nonzero count";
+    for (auto v : p.nnz_out) if (v < 0) return "negative output nonzero count";
+
+    std::vector<int32_t> slot(static_cast<size_t>(n_w), -1);   // work slot -> current SSA value
+    std::vector<std::vector<int32_t>> stored(n_out);           // (j,k) -> SSA value, -1 = never stored
+    for (int j = 0; j < n_out; ++j) stored[j].assign(static_cast<size_t>(p.nnz_out[j]), -1);
+    std::vector<std::vector<int32_t>> input_node(n_in);        // (i,k) -> INPUT node (deduplicated)
+    for (int i = 0; i < n_in; ++i) input_node[i].assign(static_cast<size_t>(p.nnz_in[i]), -1);
+    std::unordered_map<uint64_t, int32_t> const_node;          // bit pattern -> CONST node
+    std::vector<Node>& nodes = p.nodes;
+    nodes.reserve(static_cast<size_t>(n_rows));
+
+    auto slot_ok = [&](int64_t s) { return s >= 0 && s < n_w; };
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int32_t* row = code + 5 * r;
+        const int op = row[0], o = row[1], a = row[2], b = row[3];
+        if (op < 0 || op >= OP_COUNT) return row_err(r, "unknown opcode " + std::to_string(op));
+        switch (op) {
+        case OP_CONST: {
+            if (!slot_ok(o)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+            uint64_t bits;
+            std::memcpy(&bits, &values[r], 8);
+            auto it = const_node.find(bits);
+            if (it == const_node.end()) {
+                Node nd;
+                nd.op = OP_CONST;
+                nd.imm = values[r];
+                nodes.push_back(nd);
+                it = const_node.emplace(bits, static_cast<int32_t>(nodes.size() - 1)).first;
+            }
+            slot[o] = it->second;
+            break;
+        }
+        case OP_INPUT: {
+            if (!slot_ok(o)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+            if (a < 0 || a >= n_in) return row_err(r, "input index out of range (" + std::to_string(n_in) + " inputs)");
+            if (b < 0 || b >= p.nnz_in[a]) return row_err(r, "nonzero offset out of range for input");
+            int32_t& id = input_node[a][b];
+            if (id < 0) {
+                Node nd;
+                nd.op = OP_INPUT;
+                nd.in_i = a;
+                nd.in_k = b;
+                nodes.push_back(nd);
+                id = static_cast<int32_t>(nodes.size() - 1);
+            }
+            slot[o] = id;
+            break;
+        }
+        case OP_OUTPUT: {
+            if (o < 0 || o >= n_out) return row_err(r, "output index out of range (" + std::to_string(n_out) + " outputs)");
+            if (b < 0 || b >= p.nnz_out[o]) return row_err(r, "nonzero offset out of range for output");
+            if (!slot_ok(a)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+            if (slot[a] < 0) return row_err(r, "work slot read before any write");
+            stored[o][b] = slot[a];
+            break;
+        }
+        case OP_ASSIGN: {
+            if (!slot_ok(o) || !slot_ok(a)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+            if (slot[a] < 0) return row_err(r, "work slot read before any write");
+            slot[o] = slot[a];  // exact copy: an alias, no instruction
+            break;
+        }
+        default: {
+            if (!slot_ok(o)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+            Node nd;
+            nd.op = static_cast<uint8_t>(op);
+            for (int k = 0; k < kArity[op]; ++k) {
+                const int s = row[2 + k];
+                if (!slot_ok(s)) return row_err(r, "work index out of range (n_w=" + std::to_string(n_w) + ")");
+                if (slot[s] < 0) return row_err(r, "work slot read before any write");
+                nd.arg[k] = slot[s];
+            }
+            nodes.push_back(nd);
+            slot[o] = static_cast<int32_t>(nodes.size() - 1);
+            ++p.n_arith_rows;
+            break;
+        }
+        }
+    }
+    // ASSIGN rows count as arithmetic in nothing (bench.py:50-52); others already counted
+
+    // dead-code elimination: only values reaching an output store survive
+    const size_t N = nodes.size();
+    std::vector<uint8_t> live(N, 0);
+    for (int j = 0; j < n_out; ++j)
+        for (auto id : stored[j]) if (id >= 0) live[id] = 1;
+    for (size_t q = N; q-- > 0;) {
+        if (!live[q]) continue;
+        const Node& nd = nodes[q];
+        if (nd.op >= OP_ASSIGN)
+            for (int k = 0; k < kArity[nd.op]; ++k) live[nd.arg[k]] = 1;
+    }
+    std::vector<int32_t> remap(N, -1);
+    std::vector<Node> kept;
+    kept.reserve(N);
+    for (size_t q = 0; q < N; ++q) {
+        const bool arith = nodes[q].op > OP_ASSIGN;
+        if (!live[q]) { if (arith) ++p.n_dead; continue; }
+        Node nd = nodes[q];
+        if (nd.op > OP_ASSIGN)
+            for (int k = 0; k < kArity[nd.op]; ++k) nd.arg[k] = remap[nd.arg[k]];
+        remap[q] = static_cast<int32_t>(kept.size());
+        kept.push_back(nd);
+        if (arith) ++p.n_live_ops;
+    }
+    nodes.swap(kept);
+    for (int j = 0; j < n_out; ++j)
+        for (int64_t k = 0; k < p.nnz_out[j]; ++k)
+            if (stored[j][k] >= 0) p.stores.push_back({j, static_cast<int32_t>(k), remap[stored[j][k]]});
+
+    p.in_base.assign(n_in + 1, 0);
+    for (int i = 0; i < n_in; ++i) p.in_base[i + 1] = p.in_base[i] + p.nnz_in[i];
+    p.out_base.assign(n_out + 1, 0);
+    for (int j = 0; j < n_out; ++j) p.out_base[j + 1] = p.out_base[j] + p.nnz_out[j];
+    *out = std::move(p);
+    return "";
+}
+
+// ---------------------------------------------------------------------------
+// emission
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct Out {
+    std::string s;
+    void put(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        int n = vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        if (n < static_cast<int>(sizeof buf)) {
+            s.append(buf, static_cast<size_t>(n));
+        } else {
+            std::string big(static_cast<size_t>(n) + 1, '\0');
+            va_start(ap, fmt);
+            vsnprintf(&big[0], big.size(), fmt, ap);
+            va_end(ap);
+            s.append(big.data(), static_cast<size_t>(n));
+        }
+    }
+};
+
+std::string literal(double v, bool f32) {
+    char buf[64];
+    if (f32) {
+        const float f = static_cast<float>(v);
+        if (std::isnan(f) || std::isinf(f)) {
+            uint32_t bits;
+            std::memcpy(&bits, &f, 4);
+            snprintf(buf, sizeof buf, "__int_as_float(0x%08xU)", bits);
+            return buf;
+        }
+        snprintf(buf, sizeof buf, "%.9g", static_cast<double>(f));
+    } else {
+        if (std::isnan(v) || std::isinf(v)) {
+            uint64_t bits;
+            std::memcpy(&bits, &v, 8);
+            snprintf(buf, sizeof buf, "__longlong_as_double(0x%016" PRIx64 "ULL)", bits);
+            return buf;
+        }
+        snprintf(buf, sizeof buf, "%.17g", v);
+    }
+    std::string t(buf);
+    if (t.find_first_of(".en") == std::string::npos) t += ".0";
+    if (f32) t += "f";
+    if (t[0] == '-') t = "(" + t + ")";
+    return t;
+}
+
+const char* kPrelude = R"(// generated by paper_2408_09662_b200 (vsb200) -- do not edit
+// one thread per instance; SSA values live in registers; I/O staged through shared memory
+template <int NNZ, int OFF, int STRIDE>
+__device__ __forceinline__ void vs_stage_in(real* __restrict__ sm, const real* __restrict__ g, int cnt) {
+    // coalesced 16-byte loads of a contiguous [rows, NNZ] tile -> padded smem rows
+    constexpr int V = 16 / (int)sizeof(real);
+    if ((reinterpret_cast<unsigned long long>(g) & 15ULL) == 0) {
+        const int nv = cnt / V;
+        for (int j = threadIdx.x; j < nv; j += VS_BS) {
+            vec_t w = __ldg(reinterpret_cast<const vec_t*>(g) + j);
+            const real* wv = reinterpret_cast<const real*>(&w);
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+                const int q = j * V + u, row = q / NNZ, col = q - row * NNZ;
+                sm[row * STRIDE + OFF + col] = wv[u];
+            }
+        }
+        for (int q = nv * V + threadIdx.x; q < cnt; q += VS_BS) {
+            const int row = q / NNZ, col = q - row * NNZ;
+            sm[row * STRIDE + OFF + col] = __ldg(g + q);
+        }
+    } else {
+        for (int q = threadIdx.x; q < cnt; q += VS_BS) {
+            const int row = q / NNZ, col = q - row * NNZ;
+            sm[row * STRIDE + OFF + col] = __ldg(g + q);
+        }
+    }
+}
+template <int NNZ, int OFF, int STRIDE>
+__device__ __forceinline__ void vs_stage_out(real* __restrict__ g, const real* __restrict__ sm, int cnt) {
+    constexpr int V = 16 / (int)sizeof(real);
+    if ((reinterpret_cast<unsigned long long>(g) & 15ULL) == 0) {
+        const int nv = cnt / V;
+        for (int j = threadIdx.x; j < nv; j += VS_BS) {
+            vec_t w;
+            real* wv = reinterpret_cast<real*>(&w);
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+                const int q = j * V + u, row = q / NNZ, col = q - row * NNZ;
+                wv[u] = sm[row * STRIDE + OFF + col];
+            }
+            reinterpret_cast<vec_t*>(g)[j] = w;
+        }
+        for (int q = nv * V + threadIdx.x; q < cnt; q += VS_BS) {
+            const int row = q / NNZ, col = q - row * NNZ;
+            g[q] = sm[row * STRIDE + OFF + col];
+        }
+    } else {
+        for (int q = threadIdx.x; q < cnt; q += VS_BS) {
+            const int row = q / NNZ, col = q - row * NNZ;
+            g[q] = sm[row * STRIDE + OFF + col];
+        }
+    }
+}
+// FMIN/FMAX: NaN loses, ties keep the first operand (_kernels.py:116-143) -- explicit
+// selects, not DMNMX, so signed-zero ties match the reference bit for bit
+__device__ __forceinline__ real vs_fmin(real x, real y) { return (x != x) ? y : (y != y) ? x : (x <= y) ? x : y; }
+__device__ __forceinline__ real vs_fmax(real x, real y) { return (x != x) ? y : (y != y) ? x : (x >= y) ? x : y; }
+)";
+
+}  // namespace
+
+Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) {
+    Kernelset ks;
+    ks.block = opt.block;
+    ks.f32 = opt.f32;
+    ks.layout = opt.layout;
+    const int64_t N = static_cast<int64_t>(p.nodes.size());
+    const int n_in = static_cast<int>(p.nnz_in.size());
+    const int n_out = static_cast<int>(p.nnz_out.size());
+    const bool f32 = opt.f32;
+    const int rsz = f32 ? 4 : 8;
+    const char* real = f32 ? "float" : "double";
+
+    // ---- chunk boundaries over node positions --------------------------------
+    // op weight per node (CONST/INPUT are free)
+    std::vector<int64_t> opcum(N + 1, 0);
+    for (int64_t q = 0; q < N; ++q) opcum[q + 1] = opcum[q] + (p.nodes[q].op > OP_ASSIGN ? 1 : 0);
+    const int64_t total_ops = opcum[N];
+    int64_t K = opt.chunk_ops;
+    if (K <= 0) K = total_ops <= 16000 ? std::max<int64_t>(total_ops, 1) : 6000;
+
+    // last use position of every value (stores count as a use at N)
+    std::vector<int64_t> last_use(N, -1);
+    for (int64_t q = 0; q < N; ++q) {
+        const Node& nd = p.nodes[q];
+        if (nd.op > OP_ASSIGN)
+            for (int k = 0; k < kArity[nd.op]; ++k) last_use[nd.arg[k]] = std::max(last_use[nd.arg[k]], q);
+    }
+    for (const Store& s : p.stores) last_use[s.node] = N;
+    // live-across count at each cut position c (values defined < c, used >= c), CONST excluded
+    std::vector<int64_t> across(N + 1, 0);
+    {
+        std::vector<int64_t> delta(N + 2, 0);
+        for (int64_t q = 0; q < N; ++q) {
+            if (p.nodes[q].op == OP_CONST || last_use[q] < 0) continue;
+            const int64_t lo = (p.nodes[q].op == OP_INPUT) ? 0 : q + 1;  // inputs are live from the start
+            if (last_use[q] >= lo) { delta[lo] += 1; delta[last_use[q] + 1] -= 1; }
+        }
+        int64_t run = 0;
+        for (int64_t c = 0; c <= N; ++c) { run += delta[c]; across[c] = run; }
+    }
+    std::vector<int64_t> cuts = {0};
+    if (total_ops > K) {
+        int64_t pos = 0;
+        while (opcum[N] - opcum[pos] > K + K / 4) {
+            // candidate window: ops in [0.75K, 1.25K] after pos
+            const int64_t lo_ops = opcum[pos] + (3 * K) / 4, hi_ops = opcum[pos] + (5 * K) / 4;
+            int64_t lo = std::lower_bound(opcum.begin(), opcum.end(), lo_ops) - opcum.begin();
+            int64_t hi = std::lower_bound(opcum.begin(), opcum.end(), hi_ops) - opcum.begin();
+            lo = std::max(lo, pos + 1);
+            hi = std::min(hi, N);
+            int64_t best = lo;
+            for (int64_t c = lo; c <= hi; ++c)
+                if (across[c] < across[best]) best = c;
+            cuts.push_back(best);
+            pos = best;
+        }
+    }
+    cuts.push_back(N);
+    const int C = static_cast<int>(cuts.size()) - 1;
+
+    // ---- chunk membership, cross-chunk values, scratch slots ------------------
+    std::vector<int32_t> def_chunk(N, -1), last_chunk(N, -1);
+    for (int c = 0; c < C; ++c)
+        for (int64_t q = cuts[c]; q < cuts[c + 1]; ++q) def_chunk[q] = c;
+    for (int64_t q = 0; q < N; ++q)
+        if (p.nodes[q].op == OP_INPUT) def_chunk[q] = 0;  // staged by the first kernel
+    for (int c = 0; c < C; ++c)
+        for (int64_t q = cuts[c]; q < cuts[c + 1]; ++q) {
+            const Node& nd = p.nodes[q];
+            if (nd.op <= OP_ASSIGN) continue;
+            for (int k = 0; k < kArity[nd.op]; ++k) {
+                const int32_t u = nd.arg[k];
+                if (p.nodes[u].op != OP_CONST) last_chunk[u] = std::max(last_chunk[u], c);
+            }
+        }
+    for (const Store& s : p.stores)
+        if (p.nodes[s.node].op != OP_CONST) last_chunk[s.node] = std::max(last_chunk[s.node], C - 1);
+    std::vector<int32_t> slot_of(N, -1);
+    {
+        // interval colouring on [def_chunk, last_chunk] (inclusive); min-heap keeps slots dense
+        std::vector<std::vector<int32_t>> born(C), dies(C);
+        for (int64_t q = 0; q < N; ++q)
+            if (def_chunk[q] >= 0 && last_chunk[q] > def_chunk[q]) {
+                born[def_chunk[q]].push_back(static_cast<int32_t>(q));
+                dies[last_chunk[q]].push_back(static_cast<int32_t>(q));
+            }
+        std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> freeq;
+        int32_t next = 0;
+        for (int c = 0; c < C; ++c) {
+            if (c > 0)
+                for (int32_t q : dies[c - 1]) freeq.push(slot_of[q]);
+            for (int32_t q : born[c]) {
+                if (!freeq.empty()) { slot_of[q] = freeq.top(); freeq.pop(); }
+                else slot_of[q] = next++;
+            }
+        }
+        ks.scratch_slots = next;
+    }
+
+    // stores grouped per defining node for "store at definition"
+    std::vector<std::vector<int32_t>> stores_of(N);
+    for (size_t s = 0; s < p.stores.size(); ++s) stores_of[p.stores[s].node].push_back(static_cast<int32_t>(s));
+
+    // ---- I/O staging decisions ------------------------------------------------
+    const int64_t ni_tot = p.in_base[n_in], no_tot = p.out_base[n_out];
+    const int64_t SI = ni_tot | 1, SO = no_tot | 1;   // odd row strides: conflict-free smem rows
+    const bool soa = opt.layout == Layout::SOA;
+    int64_t in_bytes = soa || ni_tot == 0 ? 0 : SI * opt.block * rsz;
+    int64_t out_bytes = soa || no_tot == 0 ? 0 : SO * opt.block * rsz;
+    bool stage_in = in_bytes > 0, stage_out = out_bytes > 0;
+    const bool same_kernel = (C == 1);
+    auto fits = [&]() {
+        const int64_t a = stage_in ? in_bytes : 0, b = stage_out ? out_bytes : 0;
+        return (same_kernel ? a + b : std::max(a, b)) <= opt.smem_budget;
+    };
+    if (!fits()) {
+        // keep the cheaper-to-stage side when both do not fit
+        if (stage_in && stage_out && in_bytes <= opt.smem_budget && out_bytes <= opt.smem_budget && same_kernel) {
+            if (in_bytes <= out_bytes) stage_out = false; else stage_in = false;
+        }
+        if (stage_in && in_bytes > opt.smem_budget) stage_in = false;
+        if (stage_out && out_bytes > opt.smem_budget) stage_out = false;
+    }
+
+    // ---- kernel parameter block ------------------------------------------------
+    Out hdr;
+    hdr.put("#define VS_BS %d\n", opt.block);
+    hdr.put("typedef %s real;\n", real);
+    hdr.put("typedef %s vec_t;\n", f32 ? "float4" : "double2");
+    hdr.s += kPrelude;
+    hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
+            "    long long e0, n, ld, io_ld;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
+    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld";
+
+    // ---- per-chunk bodies -------------------------------------------------------
+    std::vector<int32_t> loaded_in(N, -1);  // chunk id in which value was made available
+    for (int c = 0; c < C; ++c) {
+        Chunk ch;
+        ch.first = cuts[c];
+        ch.last = cuts[c + 1];
+        ch.ops = opcum[ch.last] - opcum[ch.first];
+        const bool first = (c == 0), last = (c == C - 1);
+        ch.stage_in = first && stage_in;
+        ch.stage_out = last && stage_out;
+        const int64_t sin_off = 0;
+        const int64_t sout_off = ch.stage_in ? SI * opt.block : 0;
+        ch.smem_bytes = (ch.stage_in ? in_bytes : 0) + (ch.stage_out ? out_bytes : 0);
+        char nbuf[96];
+        snprintf(nbuf, sizeof nbuf, "vsk_%s_c%d", tag.c_str(), c);
+        ch.name = nbuf;
+
+        Out b;
+        b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
+        b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
+        b.put("    const long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
+        b.put("    const long long e = A.e0 + t;\n");
+        b.put("    const bool ok = t < A.n;\n");
+        b.put("    (void)e; (void)ok;\n");
+        if (ks.scratch_slots > 0) b.put("    real* __restrict__ S = A.scratch + t;\n");
+        const bool need_nblk = ch.stage_in || ch.stage_out;
+        if (need_nblk) {
+            b.put("    const long long blk0 = (long long)blockIdx.x * VS_BS;\n");
+            b.put("    const int nblk = (int)((A.n - blk0) < VS_BS ? (A.n - blk0) : VS_BS);\n");
+        }
+        if (ch.stage_in) {
+            for (int i = 0; i < n_in; ++i) {
+                if (p.nnz_in[i] == 0) continue;
+                if (soa) continue;
+                b.put("    vs_stage_in<%" PRId64 ", %" PRId64 ", %" PRId64 ">(vs_smem + %" PRId64 ", A.in[%d] + (A.e0 + blk0) * %" PRId64 "LL, nblk * %" PRId64 ");\n",
+                      p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
+            }
+            b.put("    __syncthreads();\n");
+            b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sin_off, SI);
+        }
+        if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
+
+        auto opnd = [&](int32_t u) -> std::string {
+            const Node& nu = p.nodes[u];
+            if (nu.op == OP_CONST) return literal(nu.imm, f32);
+            return "v" + std::to_string(u);
+        };
+        // make value u available in this chunk (inputs, imports from scratch)
+        std::function<void(int32_t)> ensure = [&](int32_t u) {
+            const Node& nu = p.nodes[u];
+            if (nu.op == OP_CONST || loaded_in[u] == c) return;
+            loaded_in[u] = c;
+            if (def_chunk[u] < c || (nu.op == OP_INPUT && !first)) {
+                b.put("    const real v%d = S[%d * A.ld];\n", u, slot_of[u]);
+                ++ch.loads;
+                return;
+            }
+            // INPUT defined in this (first) chunk
+            if (ch.stage_in) {
+                b.put("    const real v%d = srow[%" PRId64 "];\n", u, p.in_base[nu.in_i] + nu.in_k);
+            } else if (soa) {
+                b.put("    const real v%d = ok ? __ldg(A.in[%d] + (long long)%d * A.io_ld + e) : (real)0;\n", u, nu.in_i, nu.in_k);
+            } else {
+                b.put("    const real v%d = ok ? __ldg(A.in[%d] + e * %" PRId64 "LL + %d) : (real)0;\n", u, nu.in_i,
+                      p.nnz_in[nu.in_i], nu.in_k);
+            }
+            if (slot_of[u] >= 0 && first) { b.put("    S[%d * A.ld] = v%d;\n", slot_of[u], u); ++ch.stores; }
+        };
+        auto emit_store = [&](int32_t s_idx, const std::string& val) {
+            const Store& s = p.stores[s_idx];
+            if (ch.stage_out) {
+                b.put("    orow[%" PRId64 "] = %s;\n", p.out_base[s.j] + s.k, val.c_str());
+            } else if (soa) {
+                b.put("    if (ok) A.out[%d][(long long)%d * A.io_ld + e] = %s;\n", s.j, s.k, val.c_str());
+            } else {
+                b.put("    if (ok) A.out[%d][e * %" PRId64 "LL + %d] = %s;\n", s.j, p.nnz_out[s.j], s.k, val.c_str());
+            }
+        };
+
+        if (first) {
+            // inputs needed by later chunks: export right away (coalesced scratch rows)
+            for (int64_t q = 0; q < N; ++q)
+                if (p.nodes[q].op == OP_INPUT && slot_of[q] >= 0) ensure(static_cast<int32_t>(q));
+        }
+        if (last) {
+            // values stored from earlier chunks / constants / inputs: store them up front
+            for (size_t s = 0; s < p.stores.size(); ++s) {
+                const int32_t u = p.stores[s].node;
+                const Node& nu = p.nodes[u];
+                const bool here = nu.op > OP_INPUT && def_chunk[u] == c;
+                if (here) continue;
+                ensure(u);
+                emit_store(static_cast<int32_t>(s), opnd(u));
+            }
+        }
+        for (int64_t q = ch.first; q < ch.last; ++q) {
+            const Node& nd = p.nodes[q];
+            if (nd.op <= OP_ASSIGN) continue;  // CONST literal / INPUT on demand
+            const int ar = kArity[nd.op];
+            for (int k = 0; k < ar; ++k) ensure(nd.arg[k]);
+            const std::string x = ar > 0 ? opnd(nd.arg[0]) : "", y = ar > 1 ? opnd(nd.arg[1]) : "",
+                              z = ar > 2 ? opnd(nd.arg[2]) : "";
+            const char* X = x.c_str(); const char* Y = y.c_str(); const char* Z = z.c_str();
+            const char* fs = f32 ? "f" : "";
+            std::string expr;
+            char eb[1024];
+            switch (nd.op) {
+            case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
+            case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
+            case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
+            case OP_DIV: snprintf(eb, sizeof eb, "%s / %s", X, Y); break;
+            case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
+            case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
+            case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
+            case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
+            case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
+            case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
+            case OP_SIN: snprintf(eb, sizeof eb, "sin%s(%s)", fs, X); break;
+            case OP_COS: snprintf(eb, sizeof eb, "cos%s(%s)", fs, X); break;
+            case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
+            case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
+            case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
+            case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
+            case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;
+            case OP_STEP: snprintf(eb, sizeof eb, "(%s > (real)0) ? (real)1 : (real)0", X); break;
+            case OP_IF_ELSE: snprintf(eb, sizeof eb, "(%s != (real)0) ? %s : %s", X, Y, Z); break;
+            default: snprintf(eb, sizeof eb, "%s", X); break;
+            }
+            b.put("    const real v%" PRId64 " = %s;\n", q, eb);
+            loaded_in[q] = c;
+            if (slot_of[q] >= 0) { b.put("    S[%d * A.ld] = v%" PRId64 ";\n", slot_of[q], q); ++ch.stores; }
+            if (last)
+                for (int32_t s : stores_of[q]) emit_store(s, "v" + std::to_string(q));
+        }
+        if (ch.stage_out) {
+            b.put("    __syncthreads();\n");
+            for (int j = 0; j < n_out; ++j) {
+                if (p.nnz_out[j] == 0) continue;
+                b.put("    vs_stage_out<%" PRId64 ", %" PRId64 ", %" PRId64 ">(A.out[%d] + (A.e0 + blk0) * %" PRId64 "LL, vs_smem + %" PRId64 ", nblk * %" PRId64 ");\n",
+                      p.nnz_out[j], p.out_base[j], SO, j, p.nnz_out[j], sout_off, p.nnz_out[j]);
+            }
+        }
+        b.put("}\n");
+        ch.source = hdr.s + b.s;
+        ks.chunks.push_back(std::move(ch));
+    }
+    return ks;
+}
+
+}  // namespace vsb

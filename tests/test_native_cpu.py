@@ -1,0 +1,126 @@
+"""Host-side checks of the C ABI and the code generator that need no GPU:
+the library loads and exports every declared symbol, NVRTC compiles the
+generated sm_100a kernels, and the emitted code has the promised shape."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads
+from paper_2408_09662_b200 import BatchWorkspace, InstructionTape, Plan, batch_eval, default_thread_count
+from paper_2408_09662_b200 import _native
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "vsb200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char \*)\s*\*?\s*(vsb_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _native.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) == set(_native.EXPORTS)
+    assert b"sm_100a" in L.vsb_version()
+
+
+def test_library_has_sm100a_code():
+    so = open(_native.LIB_PATH, "rb").read()
+    assert b"sm_100a" in so  # nvcc-built static kernels (kernels.cu)
+
+
+def test_plan_errors_are_value_errors():
+    # C-side validation (the reference's run_range does none: boundscheck=False)
+    L = _native.lib()
+    code = np.array([[4, 0, 0, 1, -1]], dtype=np.int32)  # ADD reads unwritten slots
+    vals = np.zeros(1)
+    nin = np.array([1], dtype=np.int64)
+    h = ctypes.c_void_p()
+    rc = L.vsb_plan_create(code.ctypes.data, vals.ctypes.data, 1, 2, nin.ctypes.data, 1, nin.ctypes.data, 1,
+                           None, ctypes.byref(h))
+    assert rc == _native.VSB_ERR_INVALID
+    assert b"instruction 0: work slot read before any write" in L.vsb_last_error()
+
+
+@pytest.mark.parametrize("name", ["example", "pendulum", "cartpole_rk4", "ldlt_12"])
+def test_nvrtc_compiles_workload_for_sm100a(name, tmp_path):
+    p = Plan(workloads.load_tape(name), cache_dir=str(tmp_path), verbose=True)
+    info = p.info
+    assert info["n_chunks"] == 1 and info["scratch_slots"] == 0
+    assert info["max_local_bytes"] == 0  # no register spills on the small tapes
+    src = p.source(0)
+    assert "work[" not in src               # no global work vector (codegen.py:29-56 shape is gone)
+    assert "fmin(" not in src.replace("vs_fmin(", "")  # select-based min/max only
+    assert "sm_100a" in p.log
+    # cache hit on the second build
+    q = Plan(workloads.load_tape(name), cache_dir=str(tmp_path))
+    assert q.info["cache_hits"] == 1 and q.info["compile_seconds"] == 0.0
+
+
+def test_ssa_drops_dead_code_and_assign():
+    rows = [
+        [1, 0, 0, 0, -1],   # x
+        [13, 1, 0, -1, -1], # SQ  (dead: overwritten before use)
+        [3, 1, 0, -1, -1],  # ASSIGN w1 = w0 (alias, no instruction)
+        [14, 0, 1, -1, -1], # SIN
+        [2, 0, 0, 0, -1],
+    ]
+    t = InstructionTape("dce", np.array(rows, dtype=np.int32), np.zeros(5), 2, [1], [1])
+    p = Plan(t, cache_dir="")
+    src = p.source(0)
+    body = src.split("srow = ")[1]
+    assert "v0 * v0" not in body and "sin(v0)" in body  # SQ eliminated, ASSIGN aliased
+    assert p.info["n_live_ops"] == 1 and p.info["n_arith_rows"] == 2
+
+
+def test_splitter_cuts_large_tapes_and_bounds_liveness():
+    t = workloads.load_tape("quad_step")
+    p = Plan(t, cache_dir="", chunk_ops=6000)
+    info = p.info
+    assert info["n_chunks"] >= 6
+    assert 0 < info["scratch_slots"] <= t.n_w + 100
+    srcs = [p.source(c) for c in range(info["n_chunks"])]
+    assert all("S[" in s for s in srcs)
+    assert p.launches_per_eval(4096) == info["n_chunks"]
+
+
+def test_workspace_contract_without_gpu():
+    t = workloads.load_tape("pendulum")
+    ws = BatchWorkspace(t, 17)
+    assert [v.shape for v in ws.inputs] == [(34,), (51,)]
+    assert [v.shape for v in ws.outputs] == [(34,), (17,)]
+    assert ws.work.shape == (17 * t.n_w,)
+    bufs = list(ws.inputs) + [ws.work] + list(ws.outputs)
+    for i in range(len(bufs)):
+        for j in range(i + 1, len(bufs)):
+            assert not np.shares_memory(bufs[i], bufs[j])
+    ws.input_matrix(0)[:, 0] = np.arange(17)
+    assert ws.inputs[0][::2].tolist() == list(range(17))
+    with pytest.raises(ValueError, match="expected 2 values, got 3"):
+        ws.set_input(0, np.zeros(3))
+    with pytest.raises(ValueError, match=r"expected shape \(17, 3\)"):
+        ws.set_input(1, np.zeros((2, 3)))
+    with pytest.raises(ValueError, match="batch_size must be >= 1"):
+        BatchWorkspace(t, 0)
+    with pytest.raises(ValueError, match="workspace/tape mismatch"):
+        batch_eval(workloads.load_tape("example"), ws)
+    with pytest.raises(ValueError, match="n_threads must be >= 1"):
+        batch_eval(t, ws, n_threads=0)
+
+
+def test_thread_count_env_override(monkeypatch):
+    monkeypatch.setenv("VECSYM_THREADS", "3")
+    assert default_thread_count() == 3
+    for bad in ("zero", "0"):
+        monkeypatch.setenv("VECSYM_THREADS", bad)
+        with pytest.raises(ValueError, match="VECSYM_THREADS"):
+            default_thread_count()
+    monkeypatch.delenv("VECSYM_THREADS")
+    assert default_thread_count() == (os.cpu_count() or 1)
