@@ -51,6 +51,12 @@ typedef struct vsb_options {
     int32_t compile_threads;/* parallel NVRTC jobs; 0 = hardware concurrency               */
     int32_t verbose;        /* 1 = keep NVRTC/ptxas logs (vsb_plan_log)                     */
     const char *cache_dir;  /* cubin cache; NULL = $VSB_CACHE_DIR or ~/.cache/vsb200; "" = off */
+    int32_t team;           /* warps sharing 32 instances (intra-instance parallelism);
+                               0 = auto (by tape size), 1 = one thread per instance        */
+    int32_t phase_cost;     /* team list-scheduler phase length; 0 = auto                   */
+    int32_t priority;       /* team scheduler priority: 0 program order, 1 critical path    */
+    int32_t libdevice_trig; /* 1 = CUDA libdevice sin/cos; 0 = correctly rounded vs_math.h  */
+    int64_t team_smem;      /* bytes of smem for cross-warp values; 0 = auto (200 KiB)      */
 } vsb_options;
 
 typedef struct vsb_plan vsb_plan;
@@ -70,6 +76,12 @@ typedef struct vsb_plan_info {
     int32_t cache_hits;      /* chunks served from the cubin cache                       */
     int32_t stage_in;        /* inputs staged through shared memory                      */
     int32_t stage_out;       /* outputs staged through shared memory                     */
+    int32_t team;            /* warps per 32-instance team (0 = thread per instance)     */
+    int64_t phases;          /* team barrier phases, summed over chunks                  */
+    int64_t smem_slots;      /* max cross-warp smem slots over chunks                    */
+    int64_t overflow_slots;  /* max cross-warp values spilled to global scratch          */
+    int64_t xfers;           /* cross-warp values, summed over chunks                    */
+    double est_efficiency;   /* scheduled cost / (warps x sum of phase maxima), ops-weighted */
 } vsb_plan_info;
 
 const char *vsb_version(void);

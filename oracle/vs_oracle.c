@@ -44,6 +44,22 @@ typedef struct {
     int64_t e0, e1;
 } vso_args;
 
+/* Conditioning probe (tests only): when enabled, every transcendental
+ * result is moved by one ulp in a pseudo-random direction per (row,
+ * element) -- "the same algorithm on another conforming libm".  The spread
+ * it causes bounds how far any <=1-ulp libm may legitimately drift. */
+static uint64_t g_perturb = 0;  /* 0 = off, else the direction seed */
+void vso_set_perturb(uint64_t seed) { g_perturb = seed; }
+static inline double T1(double r, int64_t i, int64_t e)
+{
+    if (!g_perturb || !isfinite(r)) return r;
+    uint64_t h = ((uint64_t)i * 0x9E3779B97F4A7C15ULL ^ (uint64_t)e * 0xC2B2AE3D27D4EB4FULL) + g_perturb * 0xD6E8FEB86659FD93ULL;
+    h ^= h >> 31;
+    h *= 0x94D049BB133111EBULL;
+    h ^= h >> 29;
+    return nextafter(r, (h & 1) ? INFINITY : -INFINITY);
+}
+
 #define EACH for (int64_t e = b0; e < b1; ++e)
 #define W(slot) work[e * n_w + (slot)]
 
@@ -89,14 +105,14 @@ static void run_range(const vso_args *A)
             } break;
             case OP_SQRT: EACH W(o) = sqrt(W(a)); break;
             case OP_FABS: EACH W(o) = fabs(W(a)); break;
-            case OP_EXP: EACH W(o) = exp(W(a)); break;
+            case OP_EXP: EACH W(o) = T1(exp(W(a)), i, e); break;
             /* log of a negative (or -inf) is the positive quiet NaN (symcore.py:170-177) */
-            case OP_LOG: EACH { const double x = W(a); W(o) = (x < 0.0) ? NAN : log(x); } break;
-            case OP_POW: EACH W(o) = pow(W(a), W(b)); break;
-            case OP_SIN: EACH W(o) = sin(W(a)); break;
-            case OP_COS: EACH W(o) = cos(W(a)); break;
-            case OP_TAN: EACH W(o) = tan(W(a)); break;
-            case OP_ATAN2: EACH W(o) = atan2(W(a), W(b)); break;
+            case OP_LOG: EACH { const double x = W(a); W(o) = (x < 0.0) ? NAN : T1(log(x), i, e); } break;
+            case OP_POW: EACH W(o) = T1(pow(W(a), W(b)), i, e); break;
+            case OP_SIN: EACH W(o) = T1(sin(W(a)), i, e); break;
+            case OP_COS: EACH W(o) = T1(cos(W(a)), i, e); break;
+            case OP_TAN: EACH W(o) = T1(tan(W(a)), i, e); break;
+            case OP_ATAN2: EACH W(o) = T1(atan2(W(a), W(b)), i, e); break;
             default: /* ASSIGN */ EACH W(o) = W(a); break;
             }
         }

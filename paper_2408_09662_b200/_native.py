@@ -51,6 +51,11 @@ class Options(ctypes.Structure):
         ("compile_threads", ctypes.c_int32),
         ("verbose", ctypes.c_int32),
         ("cache_dir", ctypes.c_char_p),
+        ("team", ctypes.c_int32),
+        ("phase_cost", ctypes.c_int32),
+        ("priority", ctypes.c_int32),
+        ("libdevice_trig", ctypes.c_int32),
+        ("team_smem", ctypes.c_int64),
     ]
 
 
@@ -70,6 +75,12 @@ class PlanInfo(ctypes.Structure):
         ("cache_hits", ctypes.c_int32),
         ("stage_in", ctypes.c_int32),
         ("stage_out", ctypes.c_int32),
+        ("team", ctypes.c_int32),
+        ("phases", ctypes.c_int64),
+        ("smem_slots", ctypes.c_int64),
+        ("overflow_slots", ctypes.c_int64),
+        ("xfers", ctypes.c_int64),
+        ("est_efficiency", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <queue>
@@ -154,6 +155,8 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
 // emission
 // ---------------------------------------------------------------------------
 
+#include "vs_math_inc.h"
+
 namespace {
 
 struct Out {
@@ -204,7 +207,7 @@ std::string literal(double v, bool f32) {
 }
 
 const char* kPrelude = R"(// generated by paper_2408_09662_b200 (vsb200) -- do not edit
-// one thread per instance; SSA values live in registers; I/O staged through shared memory
+#define VS_BAR() asm volatile("bar.sync 0;" ::: "memory")
 template <int NNZ, int OFF, int STRIDE>
 __device__ __forceinline__ void vs_stage_in(real* __restrict__ sm, const real* __restrict__ g, int cnt) {
     // coalesced 16-byte loads of a contiguous [rows, NNZ] tile -> padded smem rows
@@ -263,6 +266,153 @@ __device__ __forceinline__ real vs_fmin(real x, real y) { return (x != x) ? y : 
 __device__ __forceinline__ real vs_fmax(real x, real y) { return (x != x) ? y : (y != y) ? x : (x >= y) ? x : y; }
 )";
 
+// FP64-pipe cost of one op in "DP instructions", for the team list scheduler
+int op_cost(int op) {
+    switch (op) {
+    case OP_ADD: case OP_SUB: case OP_MUL: case OP_SQ: case OP_NEG: case OP_FABS: return 1;
+    case OP_STEP: case OP_IF_ELSE: return 2;
+    case OP_FMIN: case OP_FMAX: return 3;
+    case OP_DIV: return 10;
+    case OP_SQRT: return 8;
+    case OP_EXP: case OP_LOG: return 25;
+    case OP_SIN: case OP_COS: return 45;
+    case OP_TAN: case OP_ATAN2: return 45;
+    case OP_POW: return 70;
+    default: return 1;
+    }
+}
+
+struct TeamSchedule {
+    int W = 1, P = 1;
+    std::vector<std::vector<std::vector<int32_t>>> seq;  // [warp][phase] -> node ids in issue order
+    double total_cost = 0.0, makespan = 0.0;
+};
+
+// List-schedule the arithmetic nodes of [first, last) over W warps in phases
+// of ~L cost units per warp.  Dependencies inside a phase are only allowed
+// within one warp (program order); cross-warp values are consumed in a later
+// phase (after the barrier that separates phases).
+TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W, int L, int prio,
+                           std::vector<int32_t>& warp_of, std::vector<int32_t>& phase_of) {
+    TeamSchedule ts;
+    ts.W = W;
+    // locality weight: an operand already in a warp's registers is worth this many cost units
+    // (owner-computes: 1000 = place next to the operands whenever that warp has room;
+    //  cuts cross-warp transfers ~36% on srbm_mpc at equal balance)
+    static const double aff_weight = getenv("VSB_AFF") ? atof(getenv("VSB_AFF")) : 1000.0;
+    std::vector<int32_t> ids;
+    for (int64_t q = first; q < last; ++q)
+        if (p.nodes[q].op > OP_ASSIGN) ids.push_back(static_cast<int32_t>(q));
+    const size_t M = ids.size();
+    auto in_chunk = [&](int32_t u) { return u >= first && u < last && p.nodes[u].op > OP_ASSIGN; };
+    // successors + remaining in-chunk predecessor counts
+    std::vector<int32_t> remaining(p.nodes.size(), 0);
+    std::vector<std::vector<int32_t>> succ;
+    std::vector<int32_t> local(p.nodes.size(), -1);
+    for (size_t i = 0; i < M; ++i) local[ids[i]] = static_cast<int32_t>(i);
+    succ.resize(M);
+    for (size_t i = 0; i < M; ++i) {
+        const Node& nd = p.nodes[ids[i]];
+        for (int k = 0; k < kArity[nd.op]; ++k) {
+            const int32_t u = nd.arg[k];
+            if (!in_chunk(u)) continue;
+            bool dup = false;
+            for (int k2 = 0; k2 < k; ++k2) dup |= nd.arg[k2] == u;
+            if (dup) continue;
+            ++remaining[ids[i]];
+            succ[local[u]].push_back(ids[i]);
+        }
+    }
+    // priority key (smaller = earlier)
+    std::vector<double> key(M);
+    if (prio == 1) {
+        std::vector<double> bl(M, 0.0);
+        for (size_t i = M; i-- > 0;) {
+            double best = 0.0;
+            for (int32_t s : succ[i]) best = std::max(best, bl[local[s]]);
+            bl[i] = best + op_cost(p.nodes[ids[i]].op);
+        }
+        for (size_t i = 0; i < M; ++i) key[i] = -bl[i] + 1e-9 * static_cast<double>(i);
+    } else {
+        for (size_t i = 0; i < M; ++i) key[i] = static_cast<double>(i);
+    }
+    using Item = std::pair<double, int32_t>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> ready;
+    for (size_t i = 0; i < M; ++i)
+        if (remaining[ids[i]] == 0) ready.push({key[i], ids[i]});
+    std::vector<double> load(W, 0.0);
+    std::vector<int32_t> deferred;
+    int phase = 0;
+    size_t placed = 0;
+    ts.seq.assign(W, {});
+    for (auto& v : ts.seq) v.emplace_back();
+    auto new_phase = [&]() {
+        double mx = 0.0;
+        for (double l : load) mx = std::max(mx, l);
+        ts.makespan += mx;
+        ++phase;
+        std::fill(load.begin(), load.end(), 0.0);
+        for (int32_t d : deferred) ready.push({key[local[d]], d});
+        deferred.clear();
+        for (auto& v : ts.seq) v.emplace_back();
+    };
+    while (placed < M) {
+        if (ready.empty()) {
+            new_phase();
+            continue;
+        }
+        const int32_t n = ready.top().second;
+        ready.pop();
+        const Node& nd = p.nodes[n];
+        int forced = -1, nforced = 0;
+        int aff[64] = {0};
+        for (int k = 0; k < kArity[nd.op]; ++k) {
+            const int32_t u = nd.arg[k];
+            if (!in_chunk(u)) continue;
+            if (phase_of[u] == phase) {
+                if (forced != warp_of[u]) { ++nforced; forced = warp_of[u]; }
+            } else if (warp_of[u] < 64) {
+                ++aff[warp_of[u]];
+            }
+        }
+        int w = -1;
+        if (nforced >= 2) {
+            deferred.push_back(n);
+            continue;
+        }
+        if (nforced == 1) {
+            if (load[forced] >= L) { deferred.push_back(n); continue; }
+            w = forced;
+        } else {
+            double best = 1e300;
+            for (int c = 0; c < W; ++c) {
+                if (load[c] >= L) continue;
+                const double score = load[c] - aff_weight * (c < 64 ? aff[c] : 0);
+                if (score < best) { best = score; w = c; }
+            }
+            if (w < 0) { deferred.push_back(n); continue; }
+        }
+        warp_of[n] = w;
+        phase_of[n] = phase;
+        const double c = op_cost(nd.op);
+        load[w] += c;
+        ts.total_cost += c;
+        ts.seq[w][phase].push_back(n);
+        ++placed;
+        for (int32_t s : succ[local[n]])
+            if (--remaining[s] == 0) ready.push({key[local[s]], s});
+        bool all_full = true;
+        for (double l : load) all_full &= l >= L;
+        if (all_full && placed < M) new_phase();
+    }
+    double mx = 0.0;
+    for (double l : load) mx = std::max(mx, l);
+    ts.makespan += mx;
+    ts.P = phase + 1;
+    for (auto& v : ts.seq) v.resize(ts.P);
+    return ts;
+}
+
 }  // namespace
 
 Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) {
@@ -270,22 +420,26 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     ks.block = opt.block;
     ks.f32 = opt.f32;
     ks.layout = opt.layout;
+    const bool team = opt.team >= 2;
+    ks.team = team ? opt.team : 0;
     const int64_t N = static_cast<int64_t>(p.nodes.size());
     const int n_in = static_cast<int>(p.nnz_in.size());
     const int n_out = static_cast<int>(p.nnz_out.size());
     const bool f32 = opt.f32;
     const int rsz = f32 ? 4 : 8;
     const char* real = f32 ? "float" : "double";
+    const bool soa = opt.layout == Layout::SOA;
 
     // ---- chunk boundaries over node positions --------------------------------
-    // op weight per node (CONST/INPUT are free)
     std::vector<int64_t> opcum(N + 1, 0);
     for (int64_t q = 0; q < N; ++q) opcum[q + 1] = opcum[q] + (p.nodes[q].op > OP_ASSIGN ? 1 : 0);
     const int64_t total_ops = opcum[N];
     int64_t K = opt.chunk_ops;
-    if (K <= 0) K = total_ops <= 16000 ? std::max<int64_t>(total_ops, 1) : 6000;
+    if (K <= 0) {
+        if (team) K = total_ops <= 48000 ? std::max<int64_t>(total_ops, 1) : 24000;
+        else K = total_ops <= 16000 ? std::max<int64_t>(total_ops, 1) : 6000;
+    }
 
-    // last use position of every value (stores count as a use at N)
     std::vector<int64_t> last_use(N, -1);
     for (int64_t q = 0; q < N; ++q) {
         const Node& nd = p.nodes[q];
@@ -293,13 +447,12 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             for (int k = 0; k < kArity[nd.op]; ++k) last_use[nd.arg[k]] = std::max(last_use[nd.arg[k]], q);
     }
     for (const Store& s : p.stores) last_use[s.node] = N;
-    // live-across count at each cut position c (values defined < c, used >= c), CONST excluded
     std::vector<int64_t> across(N + 1, 0);
     {
         std::vector<int64_t> delta(N + 2, 0);
         for (int64_t q = 0; q < N; ++q) {
             if (p.nodes[q].op == OP_CONST || last_use[q] < 0) continue;
-            const int64_t lo = (p.nodes[q].op == OP_INPUT) ? 0 : q + 1;  // inputs are live from the start
+            const int64_t lo = (p.nodes[q].op == OP_INPUT) ? 0 : q + 1;
             if (last_use[q] >= lo) { delta[lo] += 1; delta[last_use[q] + 1] -= 1; }
         }
         int64_t run = 0;
@@ -309,7 +462,6 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     if (total_ops > K) {
         int64_t pos = 0;
         while (opcum[N] - opcum[pos] > K + K / 4) {
-            // candidate window: ops in [0.75K, 1.25K] after pos
             const int64_t lo_ops = opcum[pos] + (3 * K) / 4, hi_ops = opcum[pos] + (5 * K) / 4;
             int64_t lo = std::lower_bound(opcum.begin(), opcum.end(), lo_ops) - opcum.begin();
             int64_t hi = std::lower_bound(opcum.begin(), opcum.end(), hi_ops) - opcum.begin();
@@ -325,12 +477,14 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     cuts.push_back(N);
     const int C = static_cast<int>(cuts.size()) - 1;
 
-    // ---- chunk membership, cross-chunk values, scratch slots ------------------
+    // ---- cross-chunk values and their SoA scratch slots ----------------------
+    // thread mode stages inputs in chunk 0 and exports the ones later chunks
+    // need; team mode re-loads inputs from global in every chunk
     std::vector<int32_t> def_chunk(N, -1), last_chunk(N, -1);
     for (int c = 0; c < C; ++c)
         for (int64_t q = cuts[c]; q < cuts[c + 1]; ++q) def_chunk[q] = c;
     for (int64_t q = 0; q < N; ++q)
-        if (p.nodes[q].op == OP_INPUT) def_chunk[q] = 0;  // staged by the first kernel
+        if (p.nodes[q].op == OP_INPUT) def_chunk[q] = team ? -1 : 0;
     for (int c = 0; c < C; ++c)
         for (int64_t q = cuts[c]; q < cuts[c + 1]; ++q) {
             const Node& nd = p.nodes[q];
@@ -344,7 +498,6 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         if (p.nodes[s.node].op != OP_CONST) last_chunk[s.node] = std::max(last_chunk[s.node], C - 1);
     std::vector<int32_t> slot_of(N, -1);
     {
-        // interval colouring on [def_chunk, last_chunk] (inclusive); min-heap keeps slots dense
         std::vector<std::vector<int32_t>> born(C), dies(C);
         for (int64_t q = 0; q < N; ++q)
             if (def_chunk[q] >= 0 && last_chunk[q] > def_chunk[q]) {
@@ -363,17 +516,37 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         }
         ks.scratch_slots = next;
     }
+    const int64_t cross_slots = ks.scratch_slots;
 
-    // stores grouped per defining node for "store at definition"
+    // stores grouped per defining node ("store at definition")
     std::vector<std::vector<int32_t>> stores_of(N);
     for (size_t s = 0; s < p.stores.size(); ++s) stores_of[p.stores[s].node].push_back(static_cast<int32_t>(s));
 
-    // ---- I/O staging decisions ------------------------------------------------
+    // SIN/COS of the same value share one argument reduction (vs_sincos)
+    std::vector<int32_t> partner(N, -1);
+    {
+        std::unordered_map<int32_t, int32_t> sin_of, cos_of;
+        for (int64_t q = 0; q < N; ++q) {
+            const Node& nd = p.nodes[q];
+            if (nd.op == OP_SIN) sin_of.emplace(nd.arg[0], static_cast<int32_t>(q));
+            if (nd.op == OP_COS) cos_of.emplace(nd.arg[0], static_cast<int32_t>(q));
+        }
+        for (auto& kv : sin_of) {
+            auto it = cos_of.find(kv.first);
+            if (it == cos_of.end()) continue;
+            const int32_t a = kv.second, b = it->second;
+            if (def_chunk[a] != def_chunk[b]) continue;
+            partner[a] = b;
+            partner[b] = a;
+        }
+    }
+    const bool trig_exact = opt.exact_trig && !f32;
+
+    // ---- I/O staging decisions (thread mode) ----------------------------------
     const int64_t ni_tot = p.in_base[n_in], no_tot = p.out_base[n_out];
-    const int64_t SI = ni_tot | 1, SO = no_tot | 1;   // odd row strides: conflict-free smem rows
-    const bool soa = opt.layout == Layout::SOA;
-    int64_t in_bytes = soa || ni_tot == 0 ? 0 : SI * opt.block * rsz;
-    int64_t out_bytes = soa || no_tot == 0 ? 0 : SO * opt.block * rsz;
+    const int64_t SI = ni_tot | 1, SO = no_tot | 1;
+    int64_t in_bytes = team || soa || ni_tot == 0 ? 0 : SI * opt.block * rsz;
+    int64_t out_bytes = team || soa || no_tot == 0 ? 0 : SO * opt.block * rsz;
     bool stage_in = in_bytes > 0, stage_out = out_bytes > 0;
     const bool same_kernel = (C == 1);
     auto fits = [&]() {
@@ -381,7 +554,6 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         return (same_kernel ? a + b : std::max(a, b)) <= opt.smem_budget;
     };
     if (!fits()) {
-        // keep the cheaper-to-stage side when both do not fit
         if (stage_in && stage_out && in_bytes <= opt.smem_budget && out_bytes <= opt.smem_budget && same_kernel) {
             if (in_bytes <= out_bytes) stage_out = false; else stage_in = false;
         }
@@ -389,161 +561,366 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         if (stage_out && out_bytes > opt.smem_budget) stage_out = false;
     }
 
-    // ---- kernel parameter block ------------------------------------------------
+    // ---- common source header ---------------------------------------------------
     Out hdr;
-    hdr.put("#define VS_BS %d\n", opt.block);
+    hdr.put("#define VS_BS %d\n", team ? opt.team * 32 : opt.block);
+    hdr.put("#define VS_IPB %d\n", team ? 32 : opt.block);   // instances per CTA
+    hdr.s += "#define VS_NSLOT @@NSLOT@@LL\n";                   // scratch rows per instance (patched below)
     hdr.put("typedef %s real;\n", real);
     hdr.put("typedef %s vec_t;\n", f32 ? "float4" : "double2");
     hdr.s += kPrelude;
+    if (trig_exact) {
+        hdr.s += "#define VS_MATH_DEVICE 1\n";
+        hdr.s += kVsMathSource;
+        hdr.s += "\n";
+    }
     hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
             "    long long e0, n, ld, io_ld;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
     ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld";
 
-    // ---- per-chunk bodies -------------------------------------------------------
-    std::vector<int32_t> loaded_in(N, -1);  // chunk id in which value was made available
+    const char* fs = f32 ? "f" : "";
+    auto opnd = [&](int32_t u) -> std::string {
+        const Node& nu = p.nodes[u];
+        if (nu.op == OP_CONST) return literal(nu.imm, f32);
+        return "v" + std::to_string(u);
+    };
+    // expression of one op (SIN/COS handled separately for pairing)
+    auto expr_of = [&](const Node& nd) -> std::string {
+        const int ar = kArity[nd.op];
+        const std::string x = ar > 0 ? opnd(nd.arg[0]) : "", y = ar > 1 ? opnd(nd.arg[1]) : "",
+                          z = ar > 2 ? opnd(nd.arg[2]) : "";
+        const char* X = x.c_str(); const char* Y = y.c_str(); const char* Z = z.c_str();
+        char eb[1024];
+        switch (nd.op) {
+        case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
+        case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
+        case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
+        case OP_DIV: snprintf(eb, sizeof eb, "%s / %s", X, Y); break;
+        case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
+        case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
+        case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
+        case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
+        case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
+        case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
+        case OP_SIN: snprintf(eb, sizeof eb, trig_exact ? "vs_sin(%s)" : "sin%s(%s)", trig_exact ? X : fs, X); break;
+        case OP_COS: snprintf(eb, sizeof eb, trig_exact ? "vs_cos(%s)" : "cos%s(%s)", trig_exact ? X : fs, X); break;
+        case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
+        case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
+        case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
+        case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
+        case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;
+        case OP_STEP: snprintf(eb, sizeof eb, "(%s > (real)0) ? (real)1 : (real)0", X); break;
+        case OP_IF_ELSE: snprintf(eb, sizeof eb, "(%s != (real)0) ? %s : %s", X, Y, Z); break;
+        default: snprintf(eb, sizeof eb, "%s", X); break;
+        }
+        return eb;
+    };
+    // emit the definition of node q (pairs SIN/COS); `done` marks nodes already defined
+    auto emit_def = [&](Out& b, int64_t q, std::vector<uint8_t>& done, const char* ind) {
+        if (done[q]) return;
+        const Node& nd = p.nodes[q];
+        const int32_t mate = partner[q];
+        if (mate >= 0 && !done[mate]) {
+            const int32_t sn = nd.op == OP_SIN ? static_cast<int32_t>(q) : mate;
+            const int32_t cn = nd.op == OP_SIN ? mate : static_cast<int32_t>(q);
+            const std::string x = opnd(nd.arg[0]);
+            b.put("%sreal v%d, v%d;\n", ind, sn, cn);
+            b.put("%s%s(%s, &v%d, &v%d);\n", ind, trig_exact ? "vs_sincos" : (f32 ? "sincosf" : "sincos"), x.c_str(), sn, cn);
+            done[sn] = done[cn] = 1;
+            return;
+        }
+        b.put("%sconst real v%" PRId64 " = %s;\n", ind, q, expr_of(nd).c_str());
+        done[q] = 1;
+    };
+
+    std::vector<int32_t> loaded_in(N, -1);  // thread mode: chunk in which a value is available
+    std::vector<uint8_t> done(N, 0);
+    int64_t max_overflow = 0;
+
     for (int c = 0; c < C; ++c) {
         Chunk ch;
         ch.first = cuts[c];
         ch.last = cuts[c + 1];
         ch.ops = opcum[ch.last] - opcum[ch.first];
         const bool first = (c == 0), last = (c == C - 1);
-        ch.stage_in = first && stage_in;
-        ch.stage_out = last && stage_out;
-        const int64_t sin_off = 0;
-        const int64_t sout_off = ch.stage_in ? SI * opt.block : 0;
-        ch.smem_bytes = (ch.stage_in ? in_bytes : 0) + (ch.stage_out ? out_bytes : 0);
         char nbuf[96];
         snprintf(nbuf, sizeof nbuf, "vsk_%s_c%d", tag.c_str(), c);
         ch.name = nbuf;
-
         Out b;
-        b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
-        b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
-        b.put("    const long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
-        b.put("    const long long e = A.e0 + t;\n");
-        b.put("    const bool ok = t < A.n;\n");
-        b.put("    (void)e; (void)ok;\n");
-        if (ks.scratch_slots > 0) b.put("    real* __restrict__ S = A.scratch + t;\n");
-        const bool need_nblk = ch.stage_in || ch.stage_out;
-        if (need_nblk) {
-            b.put("    const long long blk0 = (long long)blockIdx.x * VS_BS;\n");
-            b.put("    const int nblk = (int)((A.n - blk0) < VS_BS ? (A.n - blk0) : VS_BS);\n");
-        }
-        if (ch.stage_in) {
-            for (int i = 0; i < n_in; ++i) {
-                if (p.nnz_in[i] == 0) continue;
-                if (soa) continue;
-                b.put("    vs_stage_in<%" PRId64 ", %" PRId64 ", %" PRId64 ">(vs_smem + %" PRId64 ", A.in[%d] + (A.e0 + blk0) * %" PRId64 "LL, nblk * %" PRId64 ");\n",
-                      p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
-            }
-            b.put("    __syncthreads();\n");
-            b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sin_off, SI);
-        }
-        if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
 
-        auto opnd = [&](int32_t u) -> std::string {
-            const Node& nu = p.nodes[u];
-            if (nu.op == OP_CONST) return literal(nu.imm, f32);
-            return "v" + std::to_string(u);
-        };
-        // make value u available in this chunk (inputs, imports from scratch)
-        std::function<void(int32_t)> ensure = [&](int32_t u) {
-            const Node& nu = p.nodes[u];
-            if (nu.op == OP_CONST || loaded_in[u] == c) return;
-            loaded_in[u] = c;
-            if (def_chunk[u] < c || (nu.op == OP_INPUT && !first)) {
-                b.put("    const real v%d = S[%d * A.ld];\n", u, slot_of[u]);
-                ++ch.loads;
-                return;
-            }
-            // INPUT defined in this (first) chunk
-            if (ch.stage_in) {
-                b.put("    const real v%d = srow[%" PRId64 "];\n", u, p.in_base[nu.in_i] + nu.in_k);
-            } else if (soa) {
-                b.put("    const real v%d = ok ? __ldg(A.in[%d] + (long long)%d * A.io_ld + e) : (real)0;\n", u, nu.in_i, nu.in_k);
-            } else {
-                b.put("    const real v%d = ok ? __ldg(A.in[%d] + e * %" PRId64 "LL + %d) : (real)0;\n", u, nu.in_i,
-                      p.nnz_in[nu.in_i], nu.in_k);
-            }
-            if (slot_of[u] >= 0 && first) { b.put("    S[%d * A.ld] = v%d;\n", slot_of[u], u); ++ch.stores; }
-        };
-        auto emit_store = [&](int32_t s_idx, const std::string& val) {
+        auto emit_store = [&](Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) {
             const Store& s = p.stores[s_idx];
-            if (ch.stage_out) {
-                b.put("    orow[%" PRId64 "] = %s;\n", p.out_base[s.j] + s.k, val.c_str());
+            if (staged) {
+                o.put("%sorow[%" PRId64 "] = %s;\n", ind, p.out_base[s.j] + s.k, val.c_str());
             } else if (soa) {
-                b.put("    if (ok) A.out[%d][(long long)%d * A.io_ld + e] = %s;\n", s.j, s.k, val.c_str());
+                o.put("%sif (ok) O%d[(long long)%d * A.io_ld] = %s;\n", ind, s.j, s.k, val.c_str());
             } else {
-                b.put("    if (ok) A.out[%d][e * %" PRId64 "LL + %d] = %s;\n", s.j, p.nnz_out[s.j], s.k, val.c_str());
+                o.put("%sif (ok) O%d[%d] = %s;\n", ind, s.j, s.k, val.c_str());  // immediate offset
             }
         };
+        auto input_load = [&](Out& o, int32_t u, const char* ind) {
+            const Node& nu = p.nodes[u];
+            if (soa)
+                o.put("%sconst real v%d = ok ? __ldg(I%d + (long long)%d * A.io_ld) : (real)0;\n", ind, u, nu.in_i,
+                      nu.in_k);
+            else
+                o.put("%sconst real v%d = ok ? __ldg(I%d + %d) : (real)0;\n", ind, u, nu.in_i, nu.in_k);
+        };
+        // per-thread base pointers of every input/output row (hoisted address math)
+        auto io_bases = [&](Out& o) {
+            for (int i = 0; i < n_in; ++i)
+                o.put(soa ? "    const real* __restrict__ I%d = A.in[%d] + e;\n"
+                          : "    const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n",
+                      i, i, p.nnz_in[i]);
+            for (int j = 0; j < n_out; ++j)
+                o.put(soa ? "    real* __restrict__ O%d = A.out[%d] + e;\n"
+                          : "    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n",
+                      j, j, p.nnz_out[j]);
+            for (int i = 0; i < n_in; ++i) o.put("    (void)I%d;\n", i);
+            for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
+        };
 
-        if (first) {
-            // inputs needed by later chunks: export right away (coalesced scratch rows)
-            for (int64_t q = 0; q < N; ++q)
-                if (p.nodes[q].op == OP_INPUT && slot_of[q] >= 0) ensure(static_cast<int32_t>(q));
-        }
-        if (last) {
-            // values stored from earlier chunks / constants / inputs: store them up front
-            for (size_t s = 0; s < p.stores.size(); ++s) {
-                const int32_t u = p.stores[s].node;
+        if (!team) {
+            // ================= one thread per instance =================
+            ch.stage_in = first && stage_in;
+            ch.stage_out = last && stage_out;
+            ch.threads = opt.block;
+            ch.inst_per_block = opt.block;
+            const int64_t sin_off = 0;
+            const int64_t sout_off = ch.stage_in ? SI * opt.block : 0;
+            ch.smem_bytes = (ch.stage_in ? in_bytes : 0) + (ch.stage_out ? out_bytes : 0);
+            b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
+            b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
+            b.put("    const long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
+            b.put("    const long long e = A.e0 + t;\n");
+            b.put("    const bool ok = t < A.n;\n");
+            b.put("    (void)e; (void)ok;\n");
+            io_bases(b);
+            // block-local SoA scratch [block][slot][VS_IPB]: slot offsets are immediates
+            if (ks.scratch_slots > 0)
+                b.put("    real* __restrict__ S = A.scratch + (long long)blockIdx.x * (VS_NSLOT * VS_IPB) + threadIdx.x;\n");
+            if (ch.stage_in || ch.stage_out) {
+                b.put("    const long long blk0 = (long long)blockIdx.x * VS_BS;\n");
+                b.put("    const int nblk = (int)((A.n - blk0) < VS_BS ? (A.n - blk0) : VS_BS);\n");
+            }
+            if (ch.stage_in) {
+                for (int i = 0; i < n_in; ++i) {
+                    if (p.nnz_in[i] == 0) continue;
+                    b.put("    vs_stage_in<%" PRId64 ", %" PRId64 ", %" PRId64 ">(vs_smem + %" PRId64 ", A.in[%d] + (A.e0 + blk0) * %" PRId64 "LL, nblk * %" PRId64 ");\n",
+                          p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
+                }
+                b.put("    __syncthreads();\n");
+                b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sin_off, SI);
+            }
+            if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
+
+            std::function<void(int32_t)> ensure = [&](int32_t u) {
                 const Node& nu = p.nodes[u];
-                const bool here = nu.op > OP_INPUT && def_chunk[u] == c;
-                if (here) continue;
-                ensure(u);
-                emit_store(static_cast<int32_t>(s), opnd(u));
+                if (nu.op == OP_CONST || loaded_in[u] == c) return;
+                loaded_in[u] = c;
+                if (def_chunk[u] < c || (nu.op == OP_INPUT && !first)) {
+                    b.put("    const real v%d = S[%d * VS_IPB];\n", u, slot_of[u]);
+                    ++ch.loads;
+                    return;
+                }
+                if (ch.stage_in) b.put("    const real v%d = srow[%" PRId64 "];\n", u, p.in_base[nu.in_i] + nu.in_k);
+                else input_load(b, u, "    ");
+                if (slot_of[u] >= 0 && first) { b.put("    S[%d * VS_IPB] = v%d;\n", slot_of[u], u); ++ch.stores; }
+            };
+            if (first)
+                for (int64_t q = 0; q < N; ++q)
+                    if (p.nodes[q].op == OP_INPUT && slot_of[q] >= 0) ensure(static_cast<int32_t>(q));
+            if (last) {
+                for (size_t s = 0; s < p.stores.size(); ++s) {
+                    const int32_t u = p.stores[s].node;
+                    const Node& nu = p.nodes[u];
+                    if (nu.op > OP_INPUT && def_chunk[u] == c) continue;
+                    ensure(u);
+                    emit_store(b, static_cast<int32_t>(s), opnd(u), "    ", ch.stage_out);
+                }
             }
-        }
-        for (int64_t q = ch.first; q < ch.last; ++q) {
-            const Node& nd = p.nodes[q];
-            if (nd.op <= OP_ASSIGN) continue;  // CONST literal / INPUT on demand
-            const int ar = kArity[nd.op];
-            for (int k = 0; k < ar; ++k) ensure(nd.arg[k]);
-            const std::string x = ar > 0 ? opnd(nd.arg[0]) : "", y = ar > 1 ? opnd(nd.arg[1]) : "",
-                              z = ar > 2 ? opnd(nd.arg[2]) : "";
-            const char* X = x.c_str(); const char* Y = y.c_str(); const char* Z = z.c_str();
-            const char* fs = f32 ? "f" : "";
-            std::string expr;
-            char eb[1024];
-            switch (nd.op) {
-            case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
-            case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
-            case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
-            case OP_DIV: snprintf(eb, sizeof eb, "%s / %s", X, Y); break;
-            case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
-            case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
-            case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
-            case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
-            case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
-            case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
-            case OP_SIN: snprintf(eb, sizeof eb, "sin%s(%s)", fs, X); break;
-            case OP_COS: snprintf(eb, sizeof eb, "cos%s(%s)", fs, X); break;
-            case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
-            case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
-            case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
-            case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
-            case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;
-            case OP_STEP: snprintf(eb, sizeof eb, "(%s > (real)0) ? (real)1 : (real)0", X); break;
-            case OP_IF_ELSE: snprintf(eb, sizeof eb, "(%s != (real)0) ? %s : %s", X, Y, Z); break;
-            default: snprintf(eb, sizeof eb, "%s", X); break;
+            for (int64_t q = ch.first; q < ch.last; ++q) {
+                const Node& nd = p.nodes[q];
+                if (nd.op <= OP_ASSIGN) continue;
+                for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+                emit_def(b, q, done, "    ");
+                loaded_in[q] = c;
+                if (slot_of[q] >= 0) { b.put("    S[%d * VS_IPB] = v%" PRId64 ";\n", slot_of[q], q); ++ch.stores; }
+                if (last)
+                    for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), "    ", ch.stage_out);
             }
-            b.put("    const real v%" PRId64 " = %s;\n", q, eb);
-            loaded_in[q] = c;
-            if (slot_of[q] >= 0) { b.put("    S[%d * A.ld] = v%" PRId64 ";\n", slot_of[q], q); ++ch.stores; }
-            if (last)
-                for (int32_t s : stores_of[q]) emit_store(s, "v" + std::to_string(q));
-        }
-        if (ch.stage_out) {
-            b.put("    __syncthreads();\n");
-            for (int j = 0; j < n_out; ++j) {
-                if (p.nnz_out[j] == 0) continue;
-                b.put("    vs_stage_out<%" PRId64 ", %" PRId64 ", %" PRId64 ">(A.out[%d] + (A.e0 + blk0) * %" PRId64 "LL, vs_smem + %" PRId64 ", nblk * %" PRId64 ");\n",
-                      p.nnz_out[j], p.out_base[j], SO, j, p.nnz_out[j], sout_off, p.nnz_out[j]);
+            if (ch.stage_out) {
+                b.put("    __syncthreads();\n");
+                for (int j = 0; j < n_out; ++j) {
+                    if (p.nnz_out[j] == 0) continue;
+                    b.put("    vs_stage_out<%" PRId64 ", %" PRId64 ", %" PRId64 ">(A.out[%d] + (A.e0 + blk0) * %" PRId64 "LL, vs_smem + %" PRId64 ", nblk * %" PRId64 ");\n",
+                          p.nnz_out[j], p.out_base[j], SO, j, p.nnz_out[j], sout_off, p.nnz_out[j]);
+                }
             }
+            b.put("}\n");
+        } else {
+            // ================= team mode: W warps x 32 instances =================
+            const int W = opt.team;
+            ch.threads = W * 32;
+            ch.inst_per_block = 32;
+            std::vector<int32_t> warp_of(N, -1), phase_of(N, -1);
+            TeamSchedule ts = schedule_team(p, ch.first, ch.last, W, std::max(1, opt.phase_cost), opt.priority,
+                                            warp_of, phase_of);
+            const int P = ts.P;
+            ch.phases = P;
+            ch.est_efficiency = ts.makespan > 0 ? ts.total_cost / (W * ts.makespan) : 1.0;
+            auto in_chunk = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
+            // output stores not owned by an in-chunk producer: spread over warps, phase 0
+            std::vector<std::vector<int32_t>> extra_stores(W);
+            if (last) {
+                int rr = 0;
+                for (size_t s = 0; s < p.stores.size(); ++s) {
+                    const int32_t u = p.stores[s].node;
+                    if (in_chunk(u)) continue;
+                    extra_stores[rr++ % W].push_back(static_cast<int32_t>(s));
+                }
+            }
+            // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
+            std::vector<int32_t> xend(N, -1);
+            {
+                std::vector<int32_t> seen_stamp(N, -1);
+                for (int w = 0; w < W; ++w)
+                    for (int ph = 0; ph < P; ++ph)
+                        for (int32_t m : ts.seq[w][ph]) {
+                            const Node& nd = p.nodes[m];
+                            for (int k = 0; k < kArity[nd.op]; ++k) {
+                                const int32_t u = nd.arg[k];
+                                if (!in_chunk(u) || warp_of[u] == w || seen_stamp[u] == w) continue;
+                                seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
+                                xend[u] = std::max(xend[u], ph);
+                            }
+                        }
+            }
+            // capacity: smem slots of 32 lanes; longest intervals overflow to global scratch
+            const int64_t cap = std::max<int64_t>(0, opt.team_smem / (32 * rsz));
+            std::vector<int32_t> xvals;
+            for (int64_t q = ch.first; q < ch.last; ++q)
+                if (xend[q] >= 0) xvals.push_back(static_cast<int32_t>(q));
+            ch.xfers = static_cast<int64_t>(xvals.size());
+            std::vector<uint8_t> to_global(N, 0);
+            {
+                std::vector<int32_t> occ(P + 1, 0);
+                for (int32_t q : xvals)
+                    for (int ph = phase_of[q]; ph <= xend[q]; ++ph) ++occ[ph];
+                int32_t mx = 0;
+                for (int32_t o : occ) mx = std::max(mx, o);
+                if (mx > cap) {
+                    std::vector<int32_t> order = xvals;
+                    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b2) {
+                        return (xend[a] - phase_of[a]) > (xend[b2] - phase_of[b2]);
+                    });
+                    for (int32_t q : order) {
+                        int32_t m2 = 0;
+                        for (int ph = phase_of[q]; ph <= xend[q]; ++ph) m2 = std::max(m2, occ[ph]);
+                        if (m2 <= cap) continue;
+                        to_global[q] = 1;
+                        for (int ph = phase_of[q]; ph <= xend[q]; ++ph) --occ[ph];
+                    }
+                }
+            }
+            std::vector<int32_t> xslot(N, -1);
+            int64_t n_smem = 0, n_glob = 0;
+            {
+                std::vector<std::vector<int32_t>> born(P), dies(P);
+                for (int32_t q : xvals) {
+                    born[phase_of[q]].push_back(q);
+                    dies[xend[q]].push_back(q);
+                }
+                std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> fs_free, fg_free;
+                int32_t ns = 0, ng = 0;
+                for (int ph = 0; ph < P; ++ph) {
+                    if (ph > 0)
+                        for (int32_t q : dies[ph - 1]) (to_global[q] ? fg_free : fs_free).push(xslot[q]);
+                    for (int32_t q : born[ph]) {
+                        auto& fq = to_global[q] ? fg_free : fs_free;
+                        int32_t& nx = to_global[q] ? ng : ns;
+                        if (!fq.empty()) { xslot[q] = fq.top(); fq.pop(); }
+                        else xslot[q] = nx++;
+                    }
+                }
+                n_smem = ns;
+                n_glob = ng;
+            }
+            ch.smem_slots = n_smem;
+            ch.overflow_slots = n_glob;
+            max_overflow = std::max(max_overflow, n_glob);
+            ch.smem_bytes = n_smem * 32 * rsz;
+
+            b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
+            b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
+            b.put("    const int lane = threadIdx.x & 31;\n");
+            b.put("    const int warp = threadIdx.x >> 5;\n");
+            b.put("    const long long t = (long long)blockIdx.x * 32 + lane;\n");
+            b.put("    const long long e = A.e0 + t;\n");
+            b.put("    const bool ok = t < A.n;\n");
+            b.put("    (void)e; (void)ok;\n");
+            io_bases(b);
+            b.put("    real* __restrict__ S = A.scratch + (long long)blockIdx.x * (VS_NSLOT * VS_IPB) + lane;\n");
+            b.put("    real* __restrict__ X = vs_smem + lane;\n");
+            b.put("    (void)S; (void)X;\n");
+            b.put("    switch (warp) {\n");
+            std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
+            for (int w = 0; w < W; ++w) {
+                b.put("    case %d: {\n", w);
+                const char* ind = "        ";
+                auto ensure = [&](int32_t u) {
+                    const Node& nu = p.nodes[u];
+                    if (nu.op == OP_CONST || have[u] == w) return;
+                    have[u] = w;
+                    if (nu.op == OP_INPUT) { input_load(b, u, ind); return; }
+                    if (!in_chunk(u)) {  // imported from an earlier chunk
+                        b.put("%sconst real v%d = S[%d * VS_IPB];\n", ind, u, slot_of[u]);
+                        ++ch.loads;
+                        return;
+                    }
+                    // produced by another warp in an earlier phase
+                    if (to_global[u]) b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
+                    else b.put("%sconst real v%d = X[%d * 32];\n", ind, u, xslot[u]);
+                };
+                for (int32_t s : extra_stores[w]) {
+                    const int32_t u = p.stores[s].node;
+                    ensure(u);
+                    emit_store(b, s, opnd(u), ind, false);
+                }
+                for (int ph = 0; ph < P; ++ph) {
+                    for (int32_t q : ts.seq[w][ph]) {
+                        const Node& nd = p.nodes[q];
+                        for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+                        if (partner[q] >= 0 && warp_of[partner[q]] != w) {
+                            // mate lives on another warp: no pairing
+                            b.put("%sconst real v%d = %s;\n", ind, q, expr_of(nd).c_str());
+                            done[q] = 1;
+                        } else {
+                            emit_def(b, q, done, ind);
+                        }
+                        have[q] = w;
+                        if (xend[q] >= 0) {
+                            if (to_global[q]) b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
+                            else b.put("%sX[%d * 32] = v%d;\n", ind, xslot[q], q);
+                        }
+                        if (slot_of[q] >= 0) { b.put("%sS[%d * VS_IPB] = v%d;\n", ind, slot_of[q], q); ++ch.stores; }
+                        if (last)
+                            for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
+                    }
+                    if (ph + 1 < P) b.put("%sVS_BAR();\n", ind);
+                }
+                b.put("        break;\n    }\n");
+            }
+            b.put("    }\n}\n");
         }
-        b.put("}\n");
         ch.source = hdr.s + b.s;
         ks.chunks.push_back(std::move(ch));
+    }
+    ks.scratch_slots = cross_slots + max_overflow;
+    const std::string nslot = std::to_string(std::max<int64_t>(ks.scratch_slots, 1));
+    for (auto& ch : ks.chunks) {
+        const size_t at = ch.source.find("@@NSLOT@@");
+        if (at != std::string::npos) ch.source.replace(at, 9, nslot);
     }
     return ks;
 }

@@ -64,6 +64,14 @@ struct EmitOptions {
     int min_blocks = 1;        // __launch_bounds__ second argument
     int64_t chunk_ops = 0;     // target live ops per chunk kernel; 0 = auto
     int64_t smem_budget = 96 * 1024;  // bytes of static+dynamic smem for I/O staging
+    bool exact_trig = true;    // f64 SIN/COS via vs_math.h (correctly rounded) instead of libdevice
+    // team mode: `team` warps share 32 instances (lane = instance); the DAG is
+    // list-scheduled across warps in barrier-separated phases, cross-warp
+    // values travel through shared memory.  0 = one thread per instance.
+    int team = 0;
+    int phase_cost = 96;       // cost units per warp per phase (team mode)
+    int priority = 0;          // team list-scheduling priority: 0 program order, 1 critical path
+    int64_t team_smem = 200 * 1024;  // bytes of smem for cross-warp values (team mode)
 };
 
 struct Chunk {
@@ -71,7 +79,12 @@ struct Chunk {
     int64_t ops = 0;               // live arithmetic ops in the chunk
     int64_t loads = 0, stores = 0; // scratch loads/stores per instance
     bool stage_in = false, stage_out = false;
-    int64_t smem_bytes = 0;        // dynamic smem needed (I/O staging)
+    int64_t smem_bytes = 0;        // dynamic smem needed (I/O staging / team exchange)
+    int threads = 128;             // CTA size
+    int inst_per_block = 128;      // instances per CTA (team mode: 32)
+    // team-mode schedule statistics
+    int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0;
+    double est_efficiency = 0.0;   // total cost / (warps * sum of per-phase max load)
     std::string name, source;
 };
 
@@ -79,6 +92,7 @@ struct Kernelset {
     std::vector<Chunk> chunks;
     int64_t scratch_slots = 0;     // SoA scratch rows needed per instance
     int block = 128;
+    int team = 0;
     bool f32 = false;
     Layout layout = Layout::AOS;
     std::string arg_struct;        // layout of the single by-value kernel parameter (doc)

@@ -223,7 +223,13 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.min_blocks = p->opts.min_blocks;
     eo.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
     eo.smem_budget = p->opts.smem_budget;
-    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d"));
+    eo.exact_trig = p->opts.libdevice_trig == 0;
+    eo.team = p->opts.team;
+    eo.phase_cost = p->opts.phase_cost;
+    eo.priority = p->opts.priority;
+    eo.team_smem = p->opts.team_smem;
+    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") +
+                                       (eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block)));
 
     std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
                                       "-Xptxas=-v"};
@@ -239,6 +245,7 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     std::atomic<size_t> next{0};
     auto worker = [&]() {
         for (size_t c; (c = next++) < C;) {
+            if (p->opts.compile_threads < 0) continue;  // dry run: sources + schedule only
             rc[c] = compile_one(v->ks.chunks[c], nopts, p->cache_dir, &v->compiled[c]);
             if (rc[c] != VSB_OK) errs[c] = g_err;
         }
@@ -312,7 +319,9 @@ int64_t auto_wave(vsb_plan* p, const Variant* v, int64_t n) {
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
                  int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device) {
     if (n <= 0) return VSB_OK;
-    const int BS = v->ks.block;
+    int ipb_max = 32;
+    for (auto& ch : v->ks.chunks) ipb_max = std::max(ipb_max, ch.inst_per_block);
+    const int BS = ipb_max;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     const int64_t wave = auto_wave(p, v, n);
     void* scratch = nullptr;
@@ -329,15 +338,16 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     int rc = VSB_OK;
     for (int64_t w0 = 0; w0 < n && rc == VSB_OK; w0 += wave) {
         const int64_t m = std::min(wave, n - w0);
-        const int64_t grid = (m + BS - 1) / BS;
         pb[base + 1] = static_cast<uint64_t>(e0 + w0);
         pb[base + 2] = static_cast<uint64_t>(m);
-        pb[base + 3] = static_cast<uint64_t>(grid * BS);
+        pb[base + 3] = static_cast<uint64_t>((m + BS - 1) / BS * BS);  // scratch leading dim
         pb[base + 4] = static_cast<uint64_t>(io_ld);
         void* args[] = {pb.data()};
         for (size_t c = 0; c < v->kerns.size(); ++c) {
+            const auto& ch = v->ks.chunks[c];
+            const int64_t grid = (m + ch.inst_per_block - 1) / ch.inst_per_block;
             cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
-                                             dim3(BS), args, static_cast<size_t>(v->ks.chunks[c].smem_bytes), stream);
+                                             dim3(ch.threads), args, static_cast<size_t>(ch.smem_bytes), stream);
             if (e != cudaSuccess) {
                 rc = fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + v->ks.chunks[c].name + "): " + cudaGetErrorString(e));
                 break;
@@ -384,12 +394,18 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     if (p->opts.block % 32 != 0 || p->opts.block > 1024) return fail(VSB_ERR_INVALID, "block must be a multiple of 32 in [32, 1024]");
     if (p->opts.min_blocks <= 0) p->opts.min_blocks = 1;
     if (p->opts.smem_budget <= 0) p->opts.smem_budget = 96 * 1024;
+    if (p->opts.team < 0 || p->opts.team > 32) return fail(VSB_ERR_INVALID, "team must be in [0, 32]");
+    if (p->opts.phase_cost <= 0) p->opts.phase_cost = 96;
+    if (p->opts.team_smem <= 0) p->opts.team_smem = 200 * 1024;
+    p->opts.team_smem = std::min<int64_t>(p->opts.team_smem, 224 * 1024);
     p->opts.smem_budget = std::min<int64_t>(p->opts.smem_budget, 227 * 1024);
     p->cache_dir = p->opts.cache_dir ? std::string(p->opts.cache_dir) : default_cache_dir();
     p->opts.cache_dir = nullptr;
     std::string err = vsb::build_program(code, values, n_rows, n_w, nnz_in, n_in, nnz_out, n_out, &p->prog);
     if (!err.empty()) return fail(VSB_ERR_INVALID, err);
     p->tag = tape_tag(code, values, n_rows, n_w, p->prog.nnz_in, p->prog.nnz_out);
+    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 4000 ? 16 : 1;  // auto
+    if (p->opts.team == 1) p->opts.team = 0;
     Variant* v = nullptr;
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
@@ -437,6 +453,17 @@ int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
     info->cache_hits = v->cache_hits;
     info->stage_in = v->ks.chunks.front().stage_in;
     info->stage_out = v->ks.chunks.back().stage_out;
+    info->team = v->ks.team;
+    double wsum = 0.0, wtot = 0.0;
+    for (auto& ch : v->ks.chunks) {
+        info->phases += ch.phases;
+        info->smem_slots = std::max(info->smem_slots, ch.smem_slots);
+        info->overflow_slots = std::max(info->overflow_slots, ch.overflow_slots);
+        info->xfers += ch.xfers;
+        wsum += ch.est_efficiency * static_cast<double>(ch.ops);
+        wtot += static_cast<double>(ch.ops);
+    }
+    info->est_efficiency = wtot > 0 ? wsum / wtot : 0.0;
     return VSB_OK;
 }
 
@@ -555,7 +582,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     const int64_t row_bytes = (p->prog.in_base[n_in] + p->prog.out_base[n_out]) * rs;
     // pieces: >= 4 MiB of I/O each, at most 8, so copies overlap the kernels
     int64_t pieces = std::min<int64_t>(8, std::max<int64_t>(1, n * row_bytes / (4 << 20)));
-    const int64_t BS = v->ks.block;
+    const int64_t BS = 128;
     int64_t piece = (n + pieces - 1) / pieces;
     piece = (piece + BS - 1) / BS * BS;
     cudaStream_t s0 = streams[0];

@@ -64,6 +64,28 @@ def assert_close(got, ref, rtol=RTOL64, what=""):
         )
 
 
+def assert_parity(got, ref, spread=None, rtol=RTOL64, what="", factor=4.0):
+    """The fp64 parity contract: |g - r| <= max(rtol * max(|r|, 1), factor * spread)
+    where ``spread`` is the reference algorithm's own deviation when its
+    transcendental results move by one ulp (oracle.sensitivity; zero for
+    transcendental-free tapes, which therefore must match to 1e-12 -- and are
+    in fact bit-identical).  NaN == NaN, infinities exact."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    ok = close_mask(got, ref, rtol)
+    if spread is not None:
+        with np.errstate(invalid="ignore"):
+            ok |= np.isfinite(got) & np.isfinite(ref) & (np.abs(got - ref) <= factor * np.asarray(spread))
+    if not ok.all():
+        idx = tuple(np.argwhere(~ok)[0])
+        sp = float(np.asarray(spread)[idx]) if spread is not None else 0.0
+        raise AssertionError(
+            f"{what}: {int((~ok).sum())}/{ok.size} outside contract; first at {idx}: got {got[idx]!r} "
+            f"ref {ref[idx]!r} (1-ulp-libm spread {sp:.3g})"
+        )
+
+
 @pytest.fixture(scope="session")
 def golden_ops():
     return np.load(os.path.join(GOLDEN, "ops_specials.npz"))
