@@ -404,7 +404,9 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     std::string err = vsb::build_program(code, values, n_rows, n_w, nnz_in, n_in, nnz_out, n_out, &p->prog);
     if (!err.empty()) return fail(VSB_ERR_INVALID, err);
     p->tag = tape_tag(code, values, n_rows, n_w, p->prog.nnz_in, p->prog.nnz_out);
-    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 4000 ? 16 : 1;  // auto
+    // auto: one thread per instance for small tapes; 12-warp teams above ~4k ops
+    // (srbm_mpc B=4096: team 8 / 12 / 16 = 0.504 / 0.471 / 0.485 ms, profiles/r1_sweeps.jsonl)
+    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
     Variant* v = nullptr;
     int rc = build_variant(p.get(), VSB_AOS, &v);

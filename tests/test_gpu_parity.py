@@ -255,3 +255,25 @@ def test_multi_device_sharder_single_gpu():
     single = gpu_eval(tape, ins)
     for a, b in zip(sharded, single):
         assert_bitwise_or_nan(a, b, "sharded")
+
+
+@pytest.mark.parametrize("name, steps", [("pendulum", 50), ("quad_step", 20)])
+def test_device_rollout_matches_host_loop(name, steps):
+    # quadsim.rollout_batch's host loop (quadsim.py:298-303) vs the captured device loop
+    from paper_2408_09662_b200.rollout import rollout
+
+    tape = workloads.load_tape(name)
+    B = 500
+    ins = workloads.make_inputs(name, B, seed=21)
+    traj, outs = rollout(tape, torch.tensor(ins[0], device="cuda"), [None] + [torch.tensor(v, device="cuda")
+                                                                             for v in ins[1:]], steps)
+    traj = traj.cpu().numpy()
+    state = ins[0].copy()
+    for k in range(steps):
+        res = oracle.batch_eval(tape, [state] + ins[1:], n_threads=4)
+        # trajectories of a well-conditioned map: 1-ulp libm differences may
+        # accumulate linearly over the steps
+        assert_close(traj[:, k + 1], res[0], RTOL64 * 50, f"{name} step {k}")
+        for j, o in outs.items():
+            assert_close(o[:, k].cpu().numpy(), res[j], RTOL64 * 50, f"{name} step {k} out {j}")
+        state = res[0]

@@ -26,8 +26,9 @@ def time_plan(plan, tape, inputs, B, steps, warmup, dev=0):
     nin, nout = tape.nnz_in, tape.nnz_out
     in_off = np.concatenate([[0], np.cumsum(np.asarray(nin, dtype=np.int64) * B)])
     out_off = np.concatenate([[0], np.cumsum(np.asarray(nout, dtype=np.int64) * B)])
-    d_in = torch.tensor(np.concatenate([v.ravel() for v in inputs]), device="cuda")
-    d_out = torch.empty(int(out_off[-1]), dtype=torch.float64, device="cuda")
+    tdt = torch.float32 if plan.np_dtype == np.float32 else torch.float64
+    d_in = torch.tensor(np.concatenate([v.ravel() for v in inputs]), device="cuda", dtype=tdt)
+    d_out = torch.empty(int(out_off[-1]), dtype=tdt, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     s = torch.cuda.current_stream()
     for _ in range(warmup):
@@ -52,6 +53,8 @@ def main():
     ap.add_argument("--grid", nargs="*", default=[])
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--dtype", default="float64")
+    ap.add_argument("--check", type=int, default=0, help="compare N rows with the fp64 CPU oracle")
     args = ap.parse_args()
 
     import paper_2408_09662_b200 as vsb
@@ -70,16 +73,31 @@ def main():
                 opts = dict(zip(keys, combo))
                 t0 = time.time()
                 try:
-                    plan = vsb.Plan(tape, **opts)
+                    plan = vsb.Plan(tape, dtype=args.dtype, **opts)
                     info = plan.info
-                    ms, _ = time_plan(plan, tape, inputs, B, args.steps, args.warmup)
+                    ms, d_out = time_plan(plan, tape, inputs, B, args.steps, args.warmup)
                 except Exception as e:  # keep sweeping
                     print(json.dumps({"workload": name, "batch": B, "opts": opts, "error": str(e)[:500]}), flush=True)
                     continue
+                check = None
+                if args.check:
+                    import oracle
+
+                    rows = np.random.default_rng(1).choice(B, size=min(B, args.check), replace=False)
+                    ref = oracle.batch_eval(tape, [v[rows] for v in inputs], n_threads=os.cpu_count() or 1)
+                    out = d_out.double().cpu().numpy()
+                    off = np.concatenate([[0], np.cumsum(np.asarray(tape.nnz_out) * B)])
+                    errs = np.concatenate([
+                        (np.abs(out[off[j]:off[j + 1]].reshape(B, -1)[rows] - ref[j])
+                         / np.maximum(np.abs(ref[j]), 1.0)).ravel() for j in range(tape.n_out)])
+                    errs = errs[np.isfinite(errs)]
+                    check = {"rows": int(rows.size), "max_rel": float(errs.max()), "median_rel": float(np.median(errs)),
+                             "p99_rel": float(np.quantile(errs, 0.99))}
+                bpe = (4 if args.dtype == "float32" else 8) * (sum(tape.nnz_in) + sum(tape.nnz_out))
                 print(json.dumps({
-                    "workload": name, "batch": B, "opts": opts, "ms": ms, "evals_per_s": B / ms * 1e3,
-                    "fp64_tops": tape.n_arith * B / ms / 1e9,
-                    "io_gbs": 8 * (sum(tape.nnz_in) + sum(tape.nnz_out)) * B / ms / 1e6,
+                    "workload": name, "batch": B, "dtype": args.dtype, "opts": opts, "ms": ms,
+                    "evals_per_s": B / ms * 1e3, "fp64_tops": tape.n_arith * B / ms / 1e9,
+                    "io_gbs": bpe * B / ms / 1e6, "check": check,
                     "plan": {k: info[k] for k in ("n_chunks", "block", "scratch_slots", "scratch_loads",
                                                   "scratch_stores", "max_regs", "max_local_bytes",
                                                   "stage_in", "stage_out", "compile_seconds")},
