@@ -57,6 +57,13 @@ typedef struct vsb_options {
     int32_t priority;       /* team scheduler priority: 0 program order, 1 critical path    */
     int32_t libdevice_trig; /* 1 = CUDA libdevice sin/cos; 0 = correctly rounded vs_math.h  */
     int64_t team_smem;      /* bytes of smem for cross-warp values; 0 = auto (200 KiB)      */
+    int32_t groups;         /* team mode: 32-instance groups per CTA running the same warp
+                               code (instruction-fetch sharing); 0 = auto                  */
+    int32_t cluster;        /* team mode: CTAs per thread-block cluster splitting the team's
+                               warps over SMs (values cross SMs through DSMEM); 0 = auto   */
+    int32_t outline;        /* ops emitted as shared __noinline__ subroutines (one copy in the
+                               instruction cache instead of one per use): bit 0 DIV, bit 1
+                               SIN/COS; 0 = auto (team mode: both), -1 = none              */
 } vsb_options;
 
 typedef struct vsb_plan vsb_plan;
@@ -82,6 +89,9 @@ typedef struct vsb_plan_info {
     int64_t overflow_slots;  /* max cross-warp values spilled to global scratch          */
     int64_t xfers;           /* cross-warp values, summed over chunks                    */
     double est_efficiency;   /* scheduled cost / (warps x sum of phase maxima), ops-weighted */
+    int32_t groups;          /* 32-instance groups per CTA (team mode)                   */
+    int32_t cluster;         /* CTAs per cluster (team mode)                             */
+    int64_t remote_stores;   /* per-warp DSMEM stores to other CTAs, summed over chunks  */
 } vsb_plan_info;
 
 const char *vsb_version(void);

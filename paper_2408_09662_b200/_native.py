@@ -56,6 +56,9 @@ class Options(ctypes.Structure):
         ("priority", ctypes.c_int32),
         ("libdevice_trig", ctypes.c_int32),
         ("team_smem", ctypes.c_int64),
+        ("groups", ctypes.c_int32),
+        ("cluster", ctypes.c_int32),
+        ("outline", ctypes.c_int32),
     ]
 
 
@@ -81,6 +84,9 @@ class PlanInfo(ctypes.Structure):
         ("overflow_slots", ctypes.c_int64),
         ("xfers", ctypes.c_int64),
         ("est_efficiency", ctypes.c_double),
+        ("groups", ctypes.c_int32),
+        ("cluster", ctypes.c_int32),
+        ("remote_stores", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -292,7 +292,7 @@ struct TeamSchedule {
 // of ~L cost units per warp.  Dependencies inside a phase are only allowed
 // within one warp (program order); cross-warp values are consumed in a later
 // phase (after the barrier that separates phases).
-TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W, int L, int prio,
+TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W, int L, int prio, int Wl,
                            std::vector<int32_t>& warp_of, std::vector<int32_t>& phase_of) {
     TeamSchedule ts;
     ts.W = W;
@@ -300,6 +300,9 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
     // (owner-computes: 1000 = place next to the operands whenever that warp has room;
     //  cuts cross-warp transfers ~36% on srbm_mpc at equal balance)
     static const double aff_weight = getenv("VSB_AFF") ? atof(getenv("VSB_AFF")) : 1000.0;
+    // clusters: an operand held by another warp of the same CTA (same SM) avoids a DSMEM store
+    static const double rank_weight = getenv("VSB_RANK_AFF") ? atof(getenv("VSB_RANK_AFF")) : 400.0;
+    const bool ranked = Wl > 0 && Wl < W;
     std::vector<int32_t> ids;
     for (int64_t q = first; q < last; ++q)
         if (p.nodes[q].op > OP_ASSIGN) ids.push_back(static_cast<int32_t>(q));
@@ -366,6 +369,7 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
         const Node& nd = p.nodes[n];
         int forced = -1, nforced = 0;
         int aff[64] = {0};
+        int raff[64] = {0};
         for (int k = 0; k < kArity[nd.op]; ++k) {
             const int32_t u = nd.arg[k];
             if (!in_chunk(u)) continue;
@@ -373,6 +377,7 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
                 if (forced != warp_of[u]) { ++nforced; forced = warp_of[u]; }
             } else if (warp_of[u] < 64) {
                 ++aff[warp_of[u]];
+                if (ranked) ++raff[warp_of[u] / Wl];
             }
         }
         int w = -1;
@@ -387,7 +392,8 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
             double best = 1e300;
             for (int c = 0; c < W; ++c) {
                 if (load[c] >= L) continue;
-                const double score = load[c] - aff_weight * (c < 64 ? aff[c] : 0);
+                double score = load[c] - aff_weight * (c < 64 ? aff[c] : 0);
+                if (ranked) score -= rank_weight * raff[c / Wl];
                 if (score < best) { best = score; w = c; }
             }
             if (w < 0) { deferred.push_back(n); continue; }
@@ -563,20 +569,35 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
 
     // ---- common source header ---------------------------------------------------
     Out hdr;
-    hdr.put("#define VS_BS %d\n", team ? opt.team * 32 : opt.block);
-    hdr.put("#define VS_IPB %d\n", team ? 32 : opt.block);   // instances per CTA
+    const int TK = team ? std::max(1, opt.cluster) : 1;     // CTAs per cluster
+    const int TG = team ? std::max(1, opt.groups) : 1;      // instance groups per CTA
+    const int TWl = team ? opt.team / TK : 0;               // warp streams per CTA
+    ks.groups = TG;
+    ks.cluster = TK;
+    hdr.put("#define VS_BS %d\n", team ? TWl * TG * 32 : opt.block);
+    hdr.put("#define VS_IPB %d\n", team ? 32 * TG : opt.block);   // instances per CTA (team: per cluster)
     hdr.s += "#define VS_NSLOT @@NSLOT@@LL\n";                   // scratch rows per instance (patched below)
     hdr.put("typedef %s real;\n", real);
     hdr.put("typedef %s vec_t;\n", f32 ? "float4" : "double2");
     hdr.s += kPrelude;
+    if (TK > 1)
+        hdr.s += "#define VS_CBAR() asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\")\n";
     if (trig_exact) {
         hdr.s += "#define VS_MATH_DEVICE 1\n";
         hdr.s += kVsMathSource;
         hdr.s += "\n";
     }
+    const bool out_div = (opt.outline & 1) != 0;
+    const bool out_trig = (opt.outline & 2) != 0 && trig_exact;
+    if (out_div) hdr.s += "__device__ __noinline__ real vs_div_o(real a, real b) { return a / b; }\n";
+    if (out_trig)
+        hdr.s += "__device__ __noinline__ double vs_sin_o(double x) { return vs_sin(x); }\n"
+                 "__device__ __noinline__ double vs_cos_o(double x) { return vs_cos(x); }\n"
+                 "struct vs_sc { double s, c; };\n"
+                 "__device__ __noinline__ vs_sc vs_sincos_o(double x) { vs_sc r; vs_sincos(x, &r.s, &r.c); return r; }\n";
     hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
-            "    long long e0, n, ld, io_ld;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
-    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld";
+            "    long long e0, n, ld, io_ld, ipc;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
+    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc";
 
     const char* fs = f32 ? "f" : "";
     auto opnd = [&](int32_t u) -> std::string {
@@ -595,15 +616,21 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
         case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
         case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
-        case OP_DIV: snprintf(eb, sizeof eb, "%s / %s", X, Y); break;
+        case OP_DIV: snprintf(eb, sizeof eb, out_div ? "vs_div_o(%s, %s)" : "%s / %s", X, Y); break;
         case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
         case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
         case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
         case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
         case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
         case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
-        case OP_SIN: snprintf(eb, sizeof eb, trig_exact ? "vs_sin(%s)" : "sin%s(%s)", trig_exact ? X : fs, X); break;
-        case OP_COS: snprintf(eb, sizeof eb, trig_exact ? "vs_cos(%s)" : "cos%s(%s)", trig_exact ? X : fs, X); break;
+        case OP_SIN:
+            if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_sin_o(%s)" : "vs_sin(%s)", X);
+            else snprintf(eb, sizeof eb, "sin%s(%s)", fs, X);
+            break;
+        case OP_COS:
+            if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_cos_o(%s)" : "vs_cos(%s)", X);
+            else snprintf(eb, sizeof eb, "cos%s(%s)", fs, X);
+            break;
         case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
         case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
         case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
@@ -624,6 +651,12 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             const int32_t sn = nd.op == OP_SIN ? static_cast<int32_t>(q) : mate;
             const int32_t cn = nd.op == OP_SIN ? mate : static_cast<int32_t>(q);
             const std::string x = opnd(nd.arg[0]);
+            if (out_trig) {
+                b.put("%sconst vs_sc sc%d = vs_sincos_o(%s);\n", ind, sn, x.c_str());
+                b.put("%sconst real v%d = sc%d.s, v%d = sc%d.c;\n", ind, sn, sn, cn, sn);
+                done[sn] = done[cn] = 1;
+                return;
+            }
             b.put("%sreal v%d, v%d;\n", ind, sn, cn);
             b.put("%s%s(%s, &v%d, &v%d);\n", ind, trig_exact ? "vs_sincos" : (f32 ? "sincosf" : "sincos"), x.c_str(), sn, cn);
             done[sn] = done[cn] = 1;
@@ -760,12 +793,14 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             b.put("}\n");
         } else {
             // ================= team mode: W warps x 32 instances =================
-            const int W = opt.team;
-            ch.threads = W * 32;
-            ch.inst_per_block = 32;
+            const int W = opt.team, K = TK, G = TG, Wl = TWl;
+            ch.threads = Wl * G * 32;
+            ch.inst_per_block = 32 * G;
+            ch.cluster = K;
+            const int IPB = 32 * G;
             std::vector<int32_t> warp_of(N, -1), phase_of(N, -1);
             TeamSchedule ts = schedule_team(p, ch.first, ch.last, W, std::max(1, opt.phase_cost), opt.priority,
-                                            warp_of, phase_of);
+                                            K > 1 ? Wl : 0, warp_of, phase_of);
             const int P = ts.P;
             ch.phases = P;
             ch.est_efficiency = ts.makespan > 0 ? ts.total_cost / (W * ts.makespan) : 1.0;
@@ -782,6 +817,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             }
             // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
             std::vector<int32_t> xend(N, -1);
+            std::vector<uint32_t> xranks(N, 0);  // CTA ranks (of the cluster) holding consumers
             {
                 std::vector<int32_t> seen_stamp(N, -1);
                 for (int w = 0; w < W; ++w)
@@ -793,11 +829,12 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                                 if (!in_chunk(u) || warp_of[u] == w || seen_stamp[u] == w) continue;
                                 seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
                                 xend[u] = std::max(xend[u], ph);
+                                xranks[u] |= 1u << (w / Wl);
                             }
                         }
             }
             // capacity: smem slots of 32 lanes; longest intervals overflow to global scratch
-            const int64_t cap = std::max<int64_t>(0, opt.team_smem / (32 * rsz));
+            const int64_t cap = std::max<int64_t>(0, opt.team_smem / (IPB * rsz));
             std::vector<int32_t> xvals;
             for (int64_t q = ch.first; q < ch.last; ++q)
                 if (xend[q] >= 0) xvals.push_back(static_cast<int32_t>(q));
@@ -849,20 +886,43 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             ch.smem_slots = n_smem;
             ch.overflow_slots = n_glob;
             max_overflow = std::max(max_overflow, n_glob);
-            ch.smem_bytes = n_smem * 32 * rsz;
+            ch.smem_bytes = n_smem * IPB * rsz;
 
-            b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
+            if (K > 1)
+                b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", K, nbuf);
+            else
+                b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
             b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
             b.put("    const int lane = threadIdx.x & 31;\n");
-            b.put("    const int warp = threadIdx.x >> 5;\n");
-            b.put("    const long long t = (long long)blockIdx.x * 32 + lane;\n");
+            b.put("    const int wid = threadIdx.x >> 5;\n");
+            b.put("    const int grp = wid / %d;\n", Wl);
+            if (K > 1) {
+                b.put("    const int crank = (int)(blockIdx.x %% %d);\n", K);
+                b.put("    const long long cid = (long long)(blockIdx.x / %d);\n", K);
+            } else {
+                b.put("    const int crank = 0;\n");
+                b.put("    const long long cid = (long long)blockIdx.x;\n");
+            }
+            b.put("    const int warp = crank * %d + wid %% %d;\n", Wl, Wl);
+            // A.ipc <= VS_IPB instances per cluster (the runtime shrinks it so that the
+            // grid fills whole waves of SMs; the spare lanes idle)
+            b.put("    const long long t = cid * A.ipc + grp * 32 + lane;\n");
             b.put("    const long long e = A.e0 + t;\n");
-            b.put("    const bool ok = t < A.n;\n");
+            b.put("    const bool ok = (grp * 32 + lane) < A.ipc && t < A.n;\n");
             b.put("    (void)e; (void)ok;\n");
             io_bases(b);
-            b.put("    real* __restrict__ S = A.scratch + (long long)blockIdx.x * (VS_NSLOT * VS_IPB) + lane;\n");
-            b.put("    real* __restrict__ X = vs_smem + lane;\n");
+            b.put("    real* __restrict__ S = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32 + lane;\n");
+            b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");
             b.put("    (void)S; (void)X;\n");
+            if (K > 1) {
+                // shared::cluster addresses of this lane's X column in every CTA of the cluster
+                b.put("    const unsigned xl = (unsigned)__cvta_generic_to_shared(X);\n");
+                for (int r = 0; r < K; ++r)
+                    b.put("    unsigned XR%d; asm(\"mapa.shared::cluster.u32 %%0, %%1, %d;\" : \"=r\"(XR%d) : \"r\"(xl)); (void)XR%d;\n",
+                          r, r, r, r);
+                // every CTA of the cluster must be running before the first DSMEM store
+                b.put("    VS_CBAR();\n");
+            }
             b.put("    switch (warp) {\n");
             std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
             for (int w = 0; w < W; ++w) {
@@ -880,7 +940,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                     }
                     // produced by another warp in an earlier phase
                     if (to_global[u]) b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
-                    else b.put("%sconst real v%d = X[%d * 32];\n", ind, u, xslot[u]);
+                    else b.put("%sconst real v%d = X[%d * VS_IPB];\n", ind, u, xslot[u]);
                 };
                 for (int32_t s : extra_stores[w]) {
                     const int32_t u = p.stores[s].node;
@@ -900,14 +960,24 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                         }
                         have[q] = w;
                         if (xend[q] >= 0) {
-                            if (to_global[q]) b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
-                            else b.put("%sX[%d * 32] = v%d;\n", ind, xslot[q], q);
+                            if (to_global[q]) {
+                                b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
+                            } else {
+                                const int my = w / Wl;
+                                if (xranks[q] & (1u << my)) b.put("%sX[%d * VS_IPB] = v%d;\n", ind, xslot[q], q);
+                                for (int r = 0; r < K; ++r) {
+                                    if (r == my || !(xranks[q] & (1u << r))) continue;
+                                    b.put("%sasm volatile(\"st.shared::cluster.%s [%%0+%" PRId64 "], %%1;\" :: \"r\"(XR%d), \"%s\"(v%d));\n",
+                                          ind, f32 ? "f32" : "f64", static_cast<int64_t>(xslot[q]) * IPB * rsz, r, f32 ? "f" : "d", q);
+                                    ++ch.remote_stores;
+                                }
+                            }
                         }
                         if (slot_of[q] >= 0) { b.put("%sS[%d * VS_IPB] = v%d;\n", ind, slot_of[q], q); ++ch.stores; }
                         if (last)
                             for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
                     }
-                    if (ph + 1 < P) b.put("%sVS_BAR();\n", ind);
+                    if (ph + 1 < P) b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
                 }
                 b.put("        break;\n    }\n");
             }

@@ -72,6 +72,17 @@ struct EmitOptions {
     int phase_cost = 96;       // cost units per warp per phase (team mode)
     int priority = 0;          // team list-scheduling priority: 0 program order, 1 critical path
     int64_t team_smem = 200 * 1024;  // bytes of smem for cross-warp values (team mode)
+    // groups: G 32-instance groups per CTA execute the same warp code (warp =
+    // (stream, group)), so each fetched instruction is issued G times.
+    // cluster: the team's `team` warp streams are split over K CTAs of one
+    // thread-block cluster (K SMs); values crossing CTAs are stored into the
+    // consumer CTA's shared memory (DSMEM) and phases end in a cluster barrier.
+    int groups = 1;
+    int cluster = 1;
+    // bit 0: DIV, bit 1: SIN/COS emitted as calls to shared __noinline__
+    // subroutines (straight-line team code is instruction-fetch bound; one
+    // resident copy of the division / trig sequence beats one per use)
+    int outline = 0;
 };
 
 struct Chunk {
@@ -81,9 +92,10 @@ struct Chunk {
     bool stage_in = false, stage_out = false;
     int64_t smem_bytes = 0;        // dynamic smem needed (I/O staging / team exchange)
     int threads = 128;             // CTA size
-    int inst_per_block = 128;      // instances per CTA (team mode: 32)
+    int inst_per_block = 128;      // instances per CTA (cluster in team mode: 32 * groups)
+    int cluster = 1;               // CTAs per cluster (grid = clusters * cluster)
     // team-mode schedule statistics
-    int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0;
+    int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0, remote_stores = 0;
     double est_efficiency = 0.0;   // total cost / (warps * sum of per-phase max load)
     std::string name, source;
 };
@@ -92,7 +104,7 @@ struct Kernelset {
     std::vector<Chunk> chunks;
     int64_t scratch_slots = 0;     // SoA scratch rows needed per instance
     int block = 128;
-    int team = 0;
+    int team = 0, groups = 1, cluster = 1;
     bool f32 = false;
     Layout layout = Layout::AOS;
     std::string arg_struct;        // layout of the single by-value kernel parameter (doc)

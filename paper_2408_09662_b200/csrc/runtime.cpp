@@ -228,8 +228,14 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.phase_cost = p->opts.phase_cost;
     eo.priority = p->opts.priority;
     eo.team_smem = p->opts.team_smem;
-    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") +
-                                       (eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block)));
+    eo.groups = p->opts.groups;
+    eo.cluster = p->opts.cluster;
+    eo.outline = p->opts.outline < 0 ? 0 : (p->opts.outline == 0 ? (eo.team >= 2 ? 3 : 0) : p->opts.outline);
+    std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
+    if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
+        shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
+    if (eo.outline) shape += "o" + std::to_string(eo.outline);
+    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
 
     std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
                                       "-Xptxas=-v"};
@@ -315,6 +321,21 @@ int64_t auto_wave(vsb_plan* p, const Variant* v, int64_t n) {
     return std::min(n, w);
 }
 
+// instances per cluster for a launch of m instances: team kernels take up to
+// `ipb` per cluster; when the grid would leave SMs idle in its last wave, fewer
+// instances per cluster (spare lanes idle) give the same number of waves over
+// more SMs -- e.g. B=4096, 32/cluster: 128 CTAs on 148 SMs; 28/cluster: 147 CTAs
+int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
+    const vsb::Chunk& ch = ks.chunks.front();
+    const int64_t ipb = ch.inst_per_block;
+    if (ks.team < 2 || m <= 0) return ipb;  // thread mode: one thread per instance
+    const int64_t slots = std::max<int64_t>(1, n_sm / ch.cluster);  // co-resident clusters (1 CTA/SM)
+    const int64_t waves = (((m + ipb - 1) / ipb) + slots - 1) / slots;
+    int64_t ipc = (m + waves * slots - 1) / (waves * slots);
+    ipc = std::max<int64_t>(ipc, (ipb + 1) / 2);
+    return std::min(ipb, ipc);
+}
+
 // launch the kernel chain for elements [e0, e0+n) (indices relative to in/out pointers)
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
                  int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device) {
@@ -324,13 +345,19 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     const int BS = ipb_max;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     const int64_t wave = auto_wave(p, v, n);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    // every chunk of a variant has the same shape; scratch holds VS_IPB rows per cluster
+    // (or block) of the biggest launch: a full wave or the remainder wave
+    auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
     void* scratch = nullptr;
-    const int64_t ld_max = (wave + BS - 1) / BS * BS;
+    const int64_t units = std::max(units_of(wave), units_of(n % wave));
+    const int64_t ld_max = std::max<int64_t>((wave + BS - 1) / BS, units) * BS;
     if (v->ks.scratch_slots > 0) {
         ensure_pool(p, device);
         CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(ld_max * v->ks.scratch_slots * p->rsz()), stream));
     }
-    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 5), 0);
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
     for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
     for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -338,14 +365,16 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     int rc = VSB_OK;
     for (int64_t w0 = 0; w0 < n && rc == VSB_OK; w0 += wave) {
         const int64_t m = std::min(wave, n - w0);
+        const int64_t ipc = pick_ipc(v->ks, m, n_sm);
         pb[base + 1] = static_cast<uint64_t>(e0 + w0);
         pb[base + 2] = static_cast<uint64_t>(m);
         pb[base + 3] = static_cast<uint64_t>((m + BS - 1) / BS * BS);  // scratch leading dim
         pb[base + 4] = static_cast<uint64_t>(io_ld);
+        pb[base + 5] = static_cast<uint64_t>(ipc);
         void* args[] = {pb.data()};
         for (size_t c = 0; c < v->kerns.size(); ++c) {
             const auto& ch = v->ks.chunks[c];
-            const int64_t grid = (m + ch.inst_per_block - 1) / ch.inst_per_block;
+            const int64_t grid = (m + ipc - 1) / ipc * ch.cluster;
             cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
                                              dim3(ch.threads), args, static_cast<size_t>(ch.smem_bytes), stream);
             if (e != cudaSuccess) {
@@ -408,6 +437,14 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     // (srbm_mpc B=4096: team 8 / 12 / 16 = 0.504 / 0.471 / 0.485 ms, profiles/r1_sweeps.jsonl)
     if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
+    if (p->opts.groups < 0 || p->opts.groups > 32) return fail(VSB_ERR_INVALID, "groups must be in [0, 32]");
+    if (p->opts.cluster < 0 || p->opts.cluster > 16) return fail(VSB_ERR_INVALID, "cluster must be in [0, 16]");
+    if (p->opts.groups == 0) p->opts.groups = 1;
+    if (p->opts.cluster == 0) p->opts.cluster = 1;
+    if (p->opts.team == 0) { p->opts.groups = 1; p->opts.cluster = 1; }
+    if (p->opts.team % p->opts.cluster != 0) return fail(VSB_ERR_INVALID, "team must be a multiple of cluster");
+    if ((p->opts.team / p->opts.cluster) * p->opts.groups > 32)
+        return fail(VSB_ERR_INVALID, "team / cluster * groups warps exceed 1024 threads per CTA");
     Variant* v = nullptr;
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
@@ -456,12 +493,15 @@ int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
     info->stage_in = v->ks.chunks.front().stage_in;
     info->stage_out = v->ks.chunks.back().stage_out;
     info->team = v->ks.team;
+    info->groups = v->ks.groups;
+    info->cluster = v->ks.cluster;
     double wsum = 0.0, wtot = 0.0;
     for (auto& ch : v->ks.chunks) {
         info->phases += ch.phases;
         info->smem_slots = std::max(info->smem_slots, ch.smem_slots);
         info->overflow_slots = std::max(info->overflow_slots, ch.overflow_slots);
         info->xfers += ch.xfers;
+        info->remote_stores += ch.remote_stores;
         wsum += ch.est_efficiency * static_cast<double>(ch.ops);
         wtot += static_cast<double>(ch.ops);
     }

@@ -100,7 +100,9 @@ def main():
                     "io_gbs": bpe * B / ms / 1e6, "check": check,
                     "plan": {k: info[k] for k in ("n_chunks", "block", "scratch_slots", "scratch_loads",
                                                   "scratch_stores", "max_regs", "max_local_bytes",
-                                                  "stage_in", "stage_out", "compile_seconds")},
+                                                  "stage_in", "stage_out", "compile_seconds", "team", "groups",
+                                                  "cluster", "phases", "smem_slots", "overflow_slots", "xfers",
+                                                  "remote_stores", "est_efficiency")},
                     "wall_s": time.time() - t0}), flush=True)
 
 
