@@ -92,6 +92,7 @@ typedef struct vsb_plan_info {
     int32_t groups;          /* 32-instance groups per CTA (team mode)                   */
     int32_t cluster;         /* CTAs per cluster (team mode)                             */
     int64_t remote_stores;   /* per-warp DSMEM stores to other CTAs, summed over chunks  */
+    int64_t code_bytes;      /* SASS bytes (.text.*) of all chunks; /16 = instructions    */
 } vsb_plan_info;
 
 const char *vsb_version(void);

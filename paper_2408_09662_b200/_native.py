@@ -87,6 +87,7 @@ class PlanInfo(ctypes.Structure):
         ("groups", ctypes.c_int32),
         ("cluster", ctypes.c_int32),
         ("remote_stores", ctypes.c_int64),
+        ("code_bytes", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -117,7 +117,31 @@ struct CompiledChunk {
     bool cache_hit = false;
     int regs = -1;
     int64_t spill_bytes = -1;
+    int64_t code_bytes = -1;   // SASS bytes of all .text.* sections (16 B per instruction on sm_100)
 };
+
+// Sum of the .text.* section sizes of an ELF64 cubin: the kernel plus the
+// __noinline__ subroutines it calls.  In team mode each warp runs only its own
+// case of the kernel, so a CTA fetches every instruction of the chunk once;
+// this is the numerator of the instruction-fetch roofline.
+int64_t cubin_code_bytes(const std::vector<char>& elf) {
+    auto rd16 = [&](size_t o) { uint16_t v; std::memcpy(&v, elf.data() + o, 2); return v; };
+    auto rd32 = [&](size_t o) { uint32_t v; std::memcpy(&v, elf.data() + o, 4); return v; };
+    auto rd64 = [&](size_t o) { uint64_t v; std::memcpy(&v, elf.data() + o, 8); return v; };
+    if (elf.size() < 64 || std::memcmp(elf.data(), "\x7f" "ELF", 4) != 0 || elf[4] != 2) return -1;
+    const uint64_t shoff = rd64(0x28);
+    const uint16_t shentsize = rd16(0x3a), shnum = rd16(0x3c), shstrndx = rd16(0x3e);
+    if (shoff + uint64_t(shnum) * shentsize > elf.size() || shstrndx >= shnum) return -1;
+    const uint64_t stroff = rd64(shoff + uint64_t(shstrndx) * shentsize + 0x18);
+    int64_t total = 0;
+    for (uint16_t i = 0; i < shnum; ++i) {
+        const uint64_t sh = shoff + uint64_t(i) * shentsize;
+        const uint64_t name = stroff + rd32(sh);
+        if (name + 6 >= elf.size()) continue;
+        if (std::strncmp(elf.data() + name, ".text.", 6) == 0) total += static_cast<int64_t>(rd64(sh + 0x20));
+    }
+    return total;
+}
 
 std::string nvrtc_version() {
     int ma = 0, mi = 0;
@@ -127,13 +151,14 @@ std::string nvrtc_version() {
 
 // parse "Used N registers" / "N bytes spill stores" from a ptxas -v log
 void parse_ptxas(const std::string& log, CompiledChunk* c) {
+    c->code_bytes = cubin_code_bytes(c->cubin);
     auto p = log.find("Used ");
     if (p != std::string::npos) c->regs = atoi(log.c_str() + p + 5);
-    p = log.find("bytes spill stores");
-    if (p != std::string::npos) {
+    // max over the kernel and its __noinline__ subroutines
+    for (p = log.find("bytes spill stores"); p != std::string::npos; p = log.find("bytes spill stores", p + 1)) {
         size_t q = log.rfind(',', p);
         if (q == std::string::npos) q = log.rfind('\n', p);
-        c->spill_bytes = atoll(log.c_str() + (q == std::string::npos ? 0 : q + 1));
+        c->spill_bytes = std::max<int64_t>(c->spill_bytes, atoll(log.c_str() + (q == std::string::npos ? 0 : q + 1)));
     }
 }
 
@@ -329,6 +354,8 @@ int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
     const vsb::Chunk& ch = ks.chunks.front();
     const int64_t ipb = ch.inst_per_block;
     if (ks.team < 2 || m <= 0) return ipb;  // thread mode: one thread per instance
+    static const bool fill = !(getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) == 0);
+    if (!fill) return ipb;
     const int64_t slots = std::max<int64_t>(1, n_sm / ch.cluster);  // co-resident clusters (1 CTA/SM)
     const int64_t waves = (((m + ipb - 1) / ipb) + slots - 1) / slots;
     int64_t ipc = (m + waves * slots - 1) / (waves * slots);
@@ -487,6 +514,7 @@ int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
     for (auto& c : v->compiled) {
         info->max_regs = std::max(info->max_regs, c.regs);
         info->max_local_bytes = std::max(info->max_local_bytes, c.spill_bytes);
+        if (c.code_bytes > 0) info->code_bytes += c.code_bytes;
     }
     info->compile_seconds = v->compile_seconds;
     info->cache_hits = v->cache_hits;

@@ -15,7 +15,7 @@ import subprocess
 import tempfile
 
 
-def gen(ops: int, warps: int, distinct: bool, consts: bool = False) -> str:
+def gen(ops: int, warps: int, distinct: bool, consts: bool = False, shift: bool = False) -> str:
     acc = 16
     lines = ["extern \"C\" __global__ void k(double* out, double s) {",
              "  const int w = threadIdx.x >> 5;",
@@ -33,7 +33,8 @@ def gen(ops: int, warps: int, distinct: bool, consts: bool = False) -> str:
                 body.append(f"    a{r} = a{r} + b{(i // acc + w * 5 + r) % acc};")
         bodies.append(body)
     if distinct:
-        lines.append("  switch (w) {")
+        # shift: CTA c's warp w runs stream (w + c) % warps, so SMs run different code at a time
+        lines.append("  switch ((w + blockIdx.x) %% %d) {" % warps if shift else "  switch (w) {")
         for w, body in enumerate(bodies):
             lines.append(f"  case {w}: {{")
             lines += body
@@ -69,8 +70,26 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", type=int, default=20000)
     ap.add_argument("--consts", action="store_true", help="literal operands instead of registers")
+    ap.add_argument("--scale", action="store_true",
+                    help="distinct code, 16 warps/CTA, 1 CTA/SM on 8..148 SMs (is fetch per-SM or chip-wide?)")
     args = ap.parse_args()
     tmp = tempfile.mkdtemp()
+    if args.scale:
+        for shift in (False, True):
+            src = os.path.join(tmp, "k.cu")
+            with open(src, "w") as f:
+                f.write(gen(args.ops, 16, True, False, shift) + HOST)
+            exe = os.path.join(tmp, "k")
+            subprocess.run(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "--fmad=false",
+                            "-o", exe, src], check=True)
+            for ctas in (8, 16, 32, 64, 96, 128, 148, 296):
+                ms = float(subprocess.run([exe, "16", str(ctas)], capture_output=True, text=True).stdout)
+                cyc = ms * 1e-3 * 1.965e9
+                instr = args.ops * 16 * ctas
+                print(json.dumps({"mode": "scale", "shift": shift, "ctas": ctas, "ms": ms,
+                                  "instr_per_busy_sm_cycle": instr / min(ctas, 148) / cyc,
+                                  "chip_instr_per_s": instr / (ms * 1e-3)}), flush=True)
+        return
     for distinct in (False, True):
         for warps in (1, 2, 4, 8, 16):
             src = os.path.join(tmp, "k.cu")
