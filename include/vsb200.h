@@ -111,6 +111,8 @@ int vsb_plan_destroy(vsb_plan *plan);
 int vsb_plan_get_info(vsb_plan *plan, vsb_plan_info *info);
 /* Generated CUDA source of chained kernel `chunk` (NUL-terminated, owned by the plan). */
 int vsb_plan_source(vsb_plan *plan, int32_t chunk, const char **source);
+/* The compiled sm_100a cubin of chained kernel `chunk` (owned by the plan). */
+int vsb_plan_cubin(vsb_plan *plan, int32_t chunk, const void **data, int64_t *size);
 /* Compiler log of the last compile (may be empty). */
 int vsb_plan_log(vsb_plan *plan, const char **log);
 

@@ -20,7 +20,7 @@ VSB_F64, VSB_F32 = 0, 1
 # every symbol include/vsb200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "vsb_version", "vsb_last_error", "vsb_options_init", "vsb_plan_create", "vsb_plan_destroy",
-    "vsb_plan_get_info", "vsb_plan_source", "vsb_plan_log", "vsb_eval_device", "vsb_eval_device_ptrs",
+    "vsb_plan_get_info", "vsb_plan_source", "vsb_plan_cubin", "vsb_plan_log", "vsb_eval_device", "vsb_eval_device_ptrs",
     "vsb_eval_device_soa",
     "vsb_eval_host", "vsb_eval_host_sharded", "vsb_transpose", "vsb_launches_per_eval",
     "vsb_host_alloc", "vsb_host_free",
@@ -129,6 +129,7 @@ def lib() -> ctypes.CDLL:
     L.vsb_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
     L.vsb_plan_source.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_char_p)]
     L.vsb_plan_log.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p)]
+    L.vsb_plan_cubin.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(i64)]
     L.vsb_eval_device.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32, vp]
     L.vsb_eval_device_ptrs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i32, vp]
     L.vsb_eval_device_soa.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i32, vp]

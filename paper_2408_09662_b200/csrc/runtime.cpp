@@ -537,6 +537,16 @@ int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
     return VSB_OK;
 }
 
+int vsb_plan_cubin(vsb_plan* p, int32_t chunk, const void** data, int64_t* size) {
+    if (!p || !data || !size) return fail(VSB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Variant* v = p->variants.at(VSB_AOS).get();
+    if (chunk < 0 || chunk >= static_cast<int32_t>(v->compiled.size())) return fail(VSB_ERR_INVALID, "chunk out of range");
+    *data = v->compiled[chunk].cubin.data();
+    *size = static_cast<int64_t>(v->compiled[chunk].cubin.size());
+    return VSB_OK;
+}
+
 int vsb_plan_source(vsb_plan* p, int32_t chunk, const char** src) {
     if (!p || !src) return fail(VSB_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lk(p->mu);

@@ -104,6 +104,11 @@ class Plan:
         check(_native.lib().vsb_plan_source(self._h, int(chunk), ctypes.byref(s)))
         return s.value.decode()
 
+    def cubin(self, chunk: int = 0) -> bytes:
+        data, size = ctypes.c_void_p(), ctypes.c_int64()
+        check(_native.lib().vsb_plan_cubin(self._h, int(chunk), ctypes.byref(data), ctypes.byref(size)))
+        return ctypes.string_at(data.value, size.value) if size.value else b""
+
     @property
     def log(self) -> str:
         s = ctypes.c_char_p()
