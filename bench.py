@@ -170,7 +170,9 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-IFETCH_PEAK = 0.35  # distinct-per-warp SASS instr/cycle/SM, tools/ifetch_bench.py on B200 (profiles/r1_ifetch_reg.jsonl)
+# chip-wide instruction-fetch throughput for distinct per-warp code (straight-line DADD,
+# 16 warps/CTA, >=128 SMs busy): tools/ifetch_bench.py --scale, profiles/r1_ifetch_scale.jsonl
+IFETCH_PEAK = 1.04e11  # SASS instructions / s
 
 
 def ifetch_roof(plan, info, B, mean_s, clocks):
@@ -178,24 +180,21 @@ def ifetch_roof(plan, info, B, mean_s, clocks):
 
     Each warp of a team CTA runs its own slice of straight-line code, so a CTA
     fetches every instruction of its chunk kernels once per step: the work per
-    CTA is code_bytes/16 SASS instructions, and an SM streams distinct code at
-    IFETCH_PEAK instr/cycle (measured).  achieved = instructions fetched per SM
-    per cycle over the step.
+    CTA is code_bytes/16 SASS instructions.  The chip streams distinct code
+    from L2 at IFETCH_PEAK instr/s (measured), whichever SMs fetch it.
+    achieved = instructions fetched by all CTAs / step time.
     """
     if not info.get("team") or info.get("code_bytes", 0) <= 0:
         return None
-    n_sm = 148
     ipb = 32 * max(1, info.get("groups", 1))
     k = max(1, info.get("cluster", 1))
-    slots = max(1, n_sm // k)
-    waves = -(-(-(-B // ipb)) // slots)
-    ipc = min(ipb, max(-(-B // (waves * slots)), (ipb + 1) // 2))   # runtime.cpp pick_ipc
-    ctas = -(-B // ipc) * k
-    instr = info["code_bytes"] / 16
-    mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    achieved = instr * ctas / k / n_sm / (mean_s * mhz * 1e6)  # all 148 SMs: idle ones count against us
-    return {"achieved": achieved, "peak": IFETCH_PEAK, "unit": "SASS instr/cycle/SM", "frac": achieved / IFETCH_PEAK,
-            "code_instr_per_cta": instr / k, "ctas": ctas, "instances_per_cta": ipc, "sm_mhz": mhz}
+    ctas = -(-B // ipb) * k            # runtime.cpp pick_ipc (VSB_IPC_FILL off)
+    instr = info["code_bytes"] / 16    # every CTA of a cluster-free team fetches its chunks' code once
+    achieved = instr * ctas / k / mean_s
+    return {"achieved": achieved, "peak": IFETCH_PEAK, "unit": "SASS instr/s (chip-wide fetch)",
+            "frac": achieved / IFETCH_PEAK, "code_instr_per_cta": instr / k, "ctas": ctas,
+            "peak_source": "tools/ifetch_bench.py --scale on B200: distinct straight-line code per warp, "
+                           "1.03-1.09e11 instr/s with 128-296 CTAs (profiles/r1_ifetch_scale.jsonl)"}
 
 
 def committed_traffic(workload, info, B):

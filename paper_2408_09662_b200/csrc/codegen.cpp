@@ -349,9 +349,12 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
     size_t placed = 0;
     ts.seq.assign(W, {});
     for (auto& v : ts.seq) v.emplace_back();
+    static const bool dbg = getenv("VSB_SCHED_DEBUG") != nullptr;
     auto new_phase = [&]() {
-        double mx = 0.0;
-        for (double l : load) mx = std::max(mx, l);
+        double mx = 0.0, sum = 0.0;
+        for (double l : load) { mx = std::max(mx, l); sum += l; }
+        if (dbg) fprintf(stderr, "phase %d: max %.0f mean %.1f deferred %zu ready %zu\n", phase, mx, sum / W,
+                         deferred.size(), ready.size());
         ts.makespan += mx;
         ++phase;
         std::fill(load.begin(), load.end(), 0.0);

@@ -347,14 +347,17 @@ int64_t auto_wave(vsb_plan* p, const Variant* v, int64_t n) {
 }
 
 // instances per cluster for a launch of m instances: team kernels take up to
-// `ipb` per cluster; when the grid would leave SMs idle in its last wave, fewer
-// instances per cluster (spare lanes idle) give the same number of waves over
-// more SMs -- e.g. B=4096, 32/cluster: 128 CTAs on 148 SMs; 28/cluster: 147 CTAs
+// `ipb` per cluster; optionally (VSB_IPC_FILL=1), when the grid would leave SMs
+// idle in its last wave, fewer instances per cluster (spare lanes idle) give the
+// same number of waves over more SMs -- e.g. B=4096: 147 CTAs of 28 instead of 128 of 32
 int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
     const vsb::Chunk& ch = ks.chunks.front();
     const int64_t ipb = ch.inst_per_block;
     if (ks.team < 2 || m <= 0) return ipb;  // thread mode: one thread per instance
-    static const bool fill = !(getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) == 0);
+    // off by default: instruction fetch is a chip-wide budget (tools/ifetch_bench.py --scale:
+    // ~1.05e11 distinct instr/s whether 128 or 148 SMs fetch), so spreading the same
+    // instances over more CTAs only adds fetches (srbm_mpc B=4096 t16: 0.44 vs 0.40 ms)
+    static const bool fill = getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) != 0;
     if (!fill) return ipb;
     const int64_t slots = std::max<int64_t>(1, n_sm / ch.cluster);  // co-resident clusters (1 CTA/SM)
     const int64_t waves = (((m + ipb - 1) / ipb) + slots - 1) / slots;
@@ -462,7 +465,8 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     p->tag = tape_tag(code, values, n_rows, n_w, p->prog.nnz_in, p->prog.nnz_out);
     // auto: one thread per instance for small tapes; 12-warp teams above ~4k ops
     // (srbm_mpc B=4096: team 8 / 12 / 16 = 0.504 / 0.471 / 0.485 ms, profiles/r1_sweeps.jsonl)
-    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 4000 ? 12 : 1;
+    // (srbm_mpc 111k ops, B=4096, outlined DIV, profiles/r1_sweeps_r12.jsonl: team 16 / 12 = 0.402 / 0.418 ms)
+    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 40000 ? 16 : p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
     if (p->opts.groups < 0 || p->opts.groups > 32) return fail(VSB_ERR_INVALID, "groups must be in [0, 32]");
     if (p->opts.cluster < 0 || p->opts.cluster > 16) return fail(VSB_ERR_INVALID, "cluster must be in [0, 16]");
