@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <queue>
 #include <unordered_map>
 
@@ -747,7 +748,9 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                           p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
                 }
                 b.put("    __syncthreads();\n");
-                b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sin_off, SI);
+                // spare threads of the last block read the last staged row (they mirror instance n-1,
+                // whose outputs they may store when outputs are not staged)
+                b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + (threadIdx.x < nblk ? threadIdx.x : nblk - 1) * %" PRId64 ";\n", sin_off, SI);
             }
             if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
 
@@ -822,6 +825,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
             std::vector<int32_t> xend(N, -1);
             std::vector<uint32_t> xranks(N, 0);  // CTA ranks (of the cluster) holding consumers
+            std::vector<std::vector<int32_t>> xcons(getenv("VSB_PAIR_STATS") ? N : 0);
             {
                 std::vector<int32_t> seen_stamp(N, -1);
                 for (int w = 0; w < W; ++w)
@@ -834,8 +838,25 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                                 seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
                                 xend[u] = std::max(xend[u], ph);
                                 xranks[u] |= 1u << (w / Wl);
+                                if (getenv("VSB_PAIR_STATS")) xcons[u].push_back(w * 100000 + ph);
                             }
                         }
+            }
+            if (getenv("VSB_PAIR_STATS")) {
+                std::map<std::vector<int32_t>, int> sig;
+                int64_t nx = 0, lds = 0;
+                for (int64_t q = ch.first; q < ch.last; ++q) {
+                    if (xend[q] < 0) continue;
+                    std::vector<int32_t> k2 = xcons[q];
+                    std::sort(k2.begin(), k2.end());
+                    k2.push_back(warp_of[q]);
+                    k2.push_back(phase_of[q]);
+                    ++sig[k2]; ++nx; lds += static_cast<int64_t>(xcons[q].size());
+                }
+                int64_t pairs = 0, pair_lds = 0;
+                for (auto& kv : sig) { pairs += kv.second / 2; pair_lds += (kv.second / 2) * static_cast<int64_t>(kv.first.size() - 2); }
+                fprintf(stderr, "chunk %d: xfers %lld lds %lld  pairable: %lld pairs (saves %lld STS + %lld LDS)\n", c,
+                        (long long)nx, (long long)lds, (long long)pairs, (long long)pairs, (long long)pair_lds);
             }
             // capacity: smem slots of 32 lanes; longest intervals overflow to global scratch
             const int64_t cap = std::max<int64_t>(0, opt.team_smem / (IPB * rsz));
