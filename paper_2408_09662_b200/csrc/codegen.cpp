@@ -583,6 +583,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     hdr.s += "#define VS_NSLOT @@NSLOT@@LL\n";                   // scratch rows per instance (patched below)
     hdr.put("typedef %s real;\n", real);
     hdr.put("typedef %s vec_t;\n", f32 ? "float4" : "double2");
+    hdr.put("typedef %s vec2_t;\n", f32 ? "float2" : "double2");   // a paired cross-warp exchange
     hdr.s += kPrelude;
     if (TK > 1)
         hdr.s += "#define VS_CBAR() asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\")\n";
@@ -825,7 +826,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
             std::vector<int32_t> xend(N, -1);
             std::vector<uint32_t> xranks(N, 0);  // CTA ranks (of the cluster) holding consumers
-            std::vector<std::vector<int32_t>> xcons(getenv("VSB_PAIR_STATS") ? N : 0);
+            std::vector<std::vector<int32_t>> xcons(N);  // consumer warp * 100000 + first-use phase
             {
                 std::vector<int32_t> seen_stamp(N, -1);
                 for (int w = 0; w < W; ++w)
@@ -838,7 +839,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                                 seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
                                 xend[u] = std::max(xend[u], ph);
                                 xranks[u] |= 1u << (w / Wl);
-                                if (getenv("VSB_PAIR_STATS")) xcons[u].push_back(w * 100000 + ph);
+                                xcons[u].push_back(w * 100000 + ph);
                             }
                         }
             }
@@ -885,28 +886,70 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                     }
                 }
             }
-            std::vector<int32_t> xslot(N, -1);
+            // paired exchange: two smem values with the same producer warp, birth phase and
+            // (consumer warp, first-use phase) set travel as one 128-bit STS/LDS; a pair
+            // occupies two slot rows laid out [row pair][lane][2]
+            std::vector<int32_t> mate(N, -1);
+            std::vector<uint8_t> second(N, 0);
+            static const bool no_pair = getenv("VSB_NO_PAIR") != nullptr;
+            const bool pairing = opt.pair_xfers && K == 1 && !no_pair;
+            if (pairing) {
+                std::map<std::vector<int32_t>, int32_t> open;  // signature -> unpaired value
+                for (int w = 0; w < W; ++w)
+                    for (int ph = 0; ph < P; ++ph)
+                        for (int32_t q : ts.seq[w][ph]) {
+                            if (xend[q] < 0 || to_global[q]) continue;
+                            std::vector<int32_t> sig = xcons[q];
+                            static const bool relaxed = getenv("VSB_PAIR_RELAXED") != nullptr;
+                            if (relaxed) for (auto& x : sig) x /= 100000;  // consumer warps only
+                            std::sort(sig.begin(), sig.end());
+                            sig.push_back(w);
+                            sig.push_back(ph);
+                            auto it = open.find(sig);
+                            if (it == open.end()) { open.emplace(std::move(sig), q); continue; }
+                            mate[it->second] = q;
+                            mate[q] = it->second;
+                            second[q] = 1;  // defined after its mate in the producer's sequence
+                            open.erase(it);
+                        }
+            }
+            std::vector<int32_t> xslot(N, -1);   // smem row (single) / first row of the pair / global slot
             int64_t n_smem = 0, n_glob = 0;
-            {
+            auto allocate = [&]() {
+                std::fill(xslot.begin(), xslot.end(), -1);
                 std::vector<std::vector<int32_t>> born(P), dies(P);
                 for (int32_t q : xvals) {
+                    if (mate[q] >= 0 && second[q]) continue;  // the pair is allocated once, by its first value
                     born[phase_of[q]].push_back(q);
-                    dies[xend[q]].push_back(q);
+                    dies[mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]].push_back(q);
                 }
-                std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> fs_free, fg_free;
-                int32_t ns = 0, ng = 0;
+                std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> fs_free, fg_free, fp_free;
+                int32_t ns = 0, ng = 0, np = 0;
                 for (int ph = 0; ph < P; ++ph) {
                     if (ph > 0)
-                        for (int32_t q : dies[ph - 1]) (to_global[q] ? fg_free : fs_free).push(xslot[q]);
+                        for (int32_t q : dies[ph - 1])
+                            (to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free).push(xslot[q]);
                     for (int32_t q : born[ph]) {
-                        auto& fq = to_global[q] ? fg_free : fs_free;
-                        int32_t& nx = to_global[q] ? ng : ns;
+                        auto& fq = to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free;
+                        int32_t& nx = to_global[q] ? ng : mate[q] >= 0 ? np : ns;
                         if (!fq.empty()) { xslot[q] = fq.top(); fq.pop(); }
                         else xslot[q] = nx++;
                     }
                 }
-                n_smem = ns;
+                // rows: singles [0, ns), pairs ns + 2 * pair index
+                for (int32_t q : xvals)
+                    if (!to_global[q] && mate[q] >= 0 && !second[q]) xslot[q] = ns + 2 * xslot[q];
+                for (int32_t q : xvals)
+                    if (!to_global[q] && mate[q] >= 0 && second[q]) xslot[q] = xslot[mate[q]];
+                n_smem = ns + 2 * static_cast<int64_t>(np);
                 n_glob = ng;
+                ch.pairs = np;
+            };
+            allocate();
+            if (pairing && n_smem > cap) {  // separate pools fragmented past the budget: unpaired
+                std::fill(mate.begin(), mate.end(), -1);
+                std::fill(second.begin(), second.end(), 0);
+                allocate();
             }
             ch.smem_slots = n_smem;
             ch.overflow_slots = n_glob;
@@ -939,7 +982,8 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             io_bases(b);
             b.put("    real* __restrict__ S = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32 + lane;\n");
             b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");
-            b.put("    (void)S; (void)X;\n");
+            b.put("    real* __restrict__ X2 = vs_smem + (grp * 32 + lane) * 2;   // paired rows [row][lane][2]\n");
+            b.put("    (void)S; (void)X; (void)X2;\n");
             if (K > 1) {
                 // shared::cluster addresses of this lane's X column in every CTA of the cluster
                 b.put("    const unsigned xl = (unsigned)__cvta_generic_to_shared(X);\n");
@@ -965,8 +1009,16 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                         return;
                     }
                     // produced by another warp in an earlier phase
-                    if (to_global[u]) b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
-                    else b.put("%sconst real v%d = X[%d * VS_IPB];\n", ind, u, xslot[u]);
+                    if (to_global[u]) {
+                        b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
+                    } else if (mate[u] >= 0) {
+                        const int32_t a0 = second[u] ? mate[u] : u, a1 = second[u] ? u : mate[u];
+                        b.put("%sconst vec2_t p%d = *reinterpret_cast<const vec2_t*>(X2 + %d * VS_IPB);\n", ind, a0, xslot[u]);
+                        b.put("%sconst real v%d = p%d.x, v%d = p%d.y;\n", ind, a0, a0, a1, a0);
+                        have[mate[u]] = w;
+                    } else {
+                        b.put("%sconst real v%d = X[%d * VS_IPB];\n", ind, u, xslot[u]);
+                    }
                 };
                 for (int32_t s : extra_stores[w]) {
                     const int32_t u = p.stores[s].node;
@@ -990,7 +1042,13 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                                 b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
                             } else {
                                 const int my = w / Wl;
-                                if (xranks[q] & (1u << my)) b.put("%sX[%d * VS_IPB] = v%d;\n", ind, xslot[q], q);
+                                if (mate[q] >= 0) {
+                                    if (second[q])  // both defined now: one 128-bit store
+                                        b.put("%s*reinterpret_cast<vec2_t*>(X2 + %d * VS_IPB) = vec2_t{v%d, v%d};\n", ind,
+                                              xslot[q], mate[q], q);
+                                } else if (xranks[q] & (1u << my)) {
+                                    b.put("%sX[%d * VS_IPB] = v%d;\n", ind, xslot[q], q);
+                                }
                                 for (int r = 0; r < K; ++r) {
                                     if (r == my || !(xranks[q] & (1u << r))) continue;
                                     b.put("%sasm volatile(\"st.shared::cluster.%s [%%0+%" PRId64 "], %%1;\" :: \"r\"(XR%d), \"%s\"(v%d));\n",

@@ -83,6 +83,7 @@ struct EmitOptions {
     // subroutines (straight-line team code is instruction-fetch bound; one
     // resident copy of the division / trig sequence beats one per use)
     int outline = 0;
+    bool pair_xfers = true;    // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
 };
 
 struct Chunk {
@@ -95,7 +96,7 @@ struct Chunk {
     int inst_per_block = 128;      // instances per CTA (cluster in team mode: 32 * groups)
     int cluster = 1;               // CTAs per cluster (grid = clusters * cluster)
     // team-mode schedule statistics
-    int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0, remote_stores = 0;
+    int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0, remote_stores = 0, pairs = 0;
     double est_efficiency = 0.0;   // total cost / (warps * sum of per-phase max load)
     std::string name, source;
 };
