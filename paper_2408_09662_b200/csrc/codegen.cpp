@@ -209,6 +209,9 @@ std::string literal(double v, bool f32) {
 
 const char* kPrelude = R"(// generated by paper_2408_09662_b200 (vsb200) -- do not edit
 #define VS_BAR() asm volatile("bar.sync 0;" ::: "memory")
+// named barriers: sync = arrive + wait (acquire), arrive = release without waiting
+#define VS_BSYNC(id) asm volatile("bar.sync %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
+#define VS_BARV(id) asm volatile("bar.arrive %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 template <int NNZ, int OFF, int STRIDE>
 __device__ __forceinline__ void vs_stage_in(real* __restrict__ sm, const real* __restrict__ g, int cnt) {
     // coalesced 16-byte loads of a contiguous [rows, NNZ] tile -> padded smem rows
@@ -811,8 +814,74 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                                             K > 1 ? Wl : 0, warp_of, phase_of);
             const int P = ts.P;
             ch.phases = P;
+            // ---- split barriers (K == 1): every phase boundary is a named barrier
+            // (ids 1..15 round robin).  A warp *syncs* on barrier p only right before it first
+            // reads a cross-warp value it has not yet synced for; otherwise it just *arrives*
+            // (bar.arrive: release, no wait) and runs on into its next phase.  Ops of a phase
+            // that need no fresh cross-warp value are hoisted ahead of those that do.
+            static const bool no_split = getenv("VSB_NO_SPLIT") != nullptr;
+            const bool split = K == 1 && !no_split && opt.split_barriers;
+            auto in_chunk0 = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
+            auto xwarp = [&](int32_t u, int w) { return in_chunk0(u) && warp_of[u] != w; };
+            if (split) {
+                std::vector<int32_t> late_stamp(N, -1);
+                for (int w = 0; w < W; ++w)
+                    for (int ph = 1; ph < P; ++ph) {
+                        auto& sq = ts.seq[w][ph];
+                        std::vector<int32_t> early, late;
+                        const int32_t stamp = w * (P + 1) + ph;
+                        for (int32_t q : sq) {
+                            const Node& nd = p.nodes[q];
+                            bool lt = false;
+                            for (int k = 0; k < kArity[nd.op] && !lt; ++k) {
+                                const int32_t u = nd.arg[k];
+                                lt = (xwarp(u, w) && phase_of[u] >= ph - 1) || late_stamp[u] == stamp;
+                            }
+                            if (lt) { late.push_back(q); late_stamp[q] = stamp; } else early.push_back(q);
+                        }
+                        sq = early;
+                        sq.insert(sq.end(), late.begin(), late.end());
+                    }
+            }
+            // sync plan: sync_at[q] = barrier phase to bar.sync before op q; end_act[w][ph] =
+            // 0 nothing, 1 bar.arrive / 2 bar.sync on barrier ph-1 after the phase's ops;
+            // syncb[w][ph] = last barrier phase this warp synced on before phase ph's ops
+            std::vector<int32_t> sync_at(N, -1);
+            std::vector<std::vector<int8_t>> end_act(W, std::vector<int8_t>(P, 0));
+            std::vector<std::vector<int32_t>> syncb(W, std::vector<int32_t>(P, -1));
+            if (split) {
+                std::vector<int32_t> seen(N, -1);
+                for (int w = 0; w < W; ++w) {
+                    int last_synced = -1, pending = -1;
+                    for (int ph = 0; ph < P; ++ph) {
+                        syncb[w][ph] = last_synced;
+                        for (int32_t q : ts.seq[w][ph]) {
+                            const Node& nd = p.nodes[q];
+                            int need = -1;
+                            for (int k = 0; k < kArity[nd.op]; ++k) {
+                                const int32_t u = nd.arg[k];
+                                if (!xwarp(u, w) || seen[u] == w) continue;
+                                seen[u] = w;
+                                need = std::max(need, phase_of[u]);
+                            }
+                            if (need > last_synced) {   // pending (= ph - 1) >= need
+                                sync_at[q] = pending;
+                                last_synced = pending;
+                                pending = -1;
+                            }
+                            seen[q] = w;
+                        }
+                        if (pending >= 0) {
+                            const bool force = pending - last_synced >= 12;  // ids recycle every 15 phases
+                            end_act[w][ph] = force ? 2 : 1;
+                            if (force) last_synced = pending;
+                        }
+                        pending = ph;
+                    }
+                }
+            }
             ch.est_efficiency = ts.makespan > 0 ? ts.total_cost / (W * ts.makespan) : 1.0;
-            auto in_chunk = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
+            auto in_chunk = in_chunk0;
             // output stores not owned by an in-chunk producer: spread over warps, phase 0
             std::vector<std::vector<int32_t>> extra_stores(W);
             if (last) {
@@ -923,16 +992,22 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                     born[phase_of[q]].push_back(q);
                     dies[mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]].push_back(q);
                 }
-                std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> fs_free, fg_free, fp_free;
+                // free rows keyed by (last read phase, row): with split barriers a row read up to
+                // phase e may be rewritten by warp w only once w has synced on barrier >= e
+                using Fr = std::pair<int32_t, int32_t>;
+                std::priority_queue<Fr, std::vector<Fr>, std::greater<Fr>> fs_free, fg_free, fp_free;
                 int32_t ns = 0, ng = 0, np = 0;
                 for (int ph = 0; ph < P; ++ph) {
                     if (ph > 0)
-                        for (int32_t q : dies[ph - 1])
-                            (to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free).push(xslot[q]);
+                        for (int32_t q : dies[ph - 1]) {
+                            const int32_t e = mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q];
+                            (to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free).push({e, xslot[q]});
+                        }
                     for (int32_t q : born[ph]) {
                         auto& fq = to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free;
                         int32_t& nx = to_global[q] ? ng : mate[q] >= 0 ? np : ns;
-                        if (!fq.empty()) { xslot[q] = fq.top(); fq.pop(); }
+                        const int32_t ok_upto = split ? syncb[warp_of[q]][ph] : ph - 1;
+                        if (!fq.empty() && fq.top().first <= ok_upto) { xslot[q] = fq.top().second; fq.pop(); }
                         else xslot[q] = nx++;
                     }
                 }
@@ -946,9 +1021,26 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 ch.pairs = np;
             };
             allocate();
-            if (pairing && n_smem > cap) {  // separate pools fragmented past the budget: unpaired
-                std::fill(mate.begin(), mate.end(), -1);
-                std::fill(second.begin(), second.end(), 0);
+            // over the smem budget (separate pair pool, or rows held back for split-barrier WAR
+            // safety): demote the longest-lived smem values to global scratch until it fits
+            for (int iter = 0; n_smem > cap && iter < 64; ++iter) {
+                std::vector<int32_t> cand;
+                for (int32_t q : xvals)
+                    if (!to_global[q] && !(mate[q] >= 0 && second[q])) cand.push_back(q);
+                if (cand.empty()) break;
+                auto life = [&](int32_t q) { return (mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]) - phase_of[q]; };
+                std::sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b2) { return life(a) > life(b2); });
+                const size_t k = std::max<size_t>(1, static_cast<size_t>(cand.size() * std::min(0.5, 0.02 + double(n_smem - cap) / double(n_smem))));
+                for (size_t i = 0; i < k && i < cand.size(); ++i) {
+                    const int32_t q = cand[i];
+                    to_global[q] = 1;
+                    if (mate[q] >= 0) {
+                        to_global[mate[q]] = 1;
+                        second[mate[q]] = 0;
+                        mate[mate[q]] = -1;
+                        mate[q] = -1;
+                    }
+                }
                 allocate();
             }
             ch.smem_slots = n_smem;
@@ -1028,6 +1120,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 for (int ph = 0; ph < P; ++ph) {
                     for (int32_t q : ts.seq[w][ph]) {
                         const Node& nd = p.nodes[q];
+                        if (sync_at[q] >= 0) b.put("%sVS_BSYNC(%d);\n", ind, 1 + sync_at[q] % 15);
                         for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
                         if (partner[q] >= 0 && warp_of[partner[q]] != w) {
                             // mate lives on another warp: no pairing
@@ -1061,7 +1154,12 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                         if (last)
                             for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
                     }
-                    if (ph + 1 < P) b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
+                    if (split) {
+                        if (end_act[w][ph]) b.put(end_act[w][ph] == 2 ? "%sVS_BSYNC(%d);\n" : "%sVS_BARV(%d);\n", ind,
+                                                  1 + (ph - 1) % 15);
+                    } else if (ph + 1 < P) {
+                        b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
+                    }
                 }
                 b.put("        break;\n    }\n");
             }

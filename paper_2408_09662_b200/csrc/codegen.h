@@ -84,6 +84,7 @@ struct EmitOptions {
     // resident copy of the division / trig sequence beats one per use)
     int outline = 0;
     bool pair_xfers = true;    // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
+    bool split_barriers = true;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
 };
 
 struct Chunk {
