@@ -209,6 +209,63 @@ def committed_traffic(workload, info, B):
     return None, None
 
 
+SECONDARY = (("cartpole_rk4", 1_000_000), ("pendulum", 1_000_000), ("humanoid_rbd", 65536), ("srbm_mpc", 65536))
+
+
+def secondary_points(dev, local, hbm_gbs, steps=5):
+    """Other BASELINE configs at scale, device-resident, L2 flushed per step
+    (small tapes are the HBM-bound ones the metric's "% HBM roofline" is about)."""
+    import torch
+
+    import oracle
+    import paper_2408_09662_b200 as vsb
+    import workloads
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out = []
+    for name, B in SECONDARY:
+        tape = workloads.load_tape(name)
+        plan = vsb.get_plan(tape)
+        ins = workloads.make_inputs(name, B, seed=2000)
+        nin, nout = tape.nnz_in, tape.nnz_out
+        in_off = np.concatenate([[0], np.cumsum(np.asarray(nin, dtype=np.int64) * B)])
+        out_off = np.concatenate([[0], np.cumsum(np.asarray(nout, dtype=np.int64) * B)])
+        d_in = torch.tensor(np.concatenate([v.ravel() for v in ins]), device=dev)
+        d_out = torch.empty(int(out_off[-1]), dtype=torch.float64, device=dev)
+
+        def step():
+            plan.eval_device(d_in.data_ptr(), in_off, d_out.data_ptr(), out_off, 0, B, local, stream.cuda_stream)
+
+        for _ in range(3):
+            flush.zero_()
+            step()
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        t = statistics.median(ms) / 1e3
+        rows = np.random.default_rng(0).choice(B, size=16, replace=False)
+        ref = oracle.batch_eval(tape, [v[rows] for v in ins])
+        got = d_out.cpu().numpy()
+        worst = 0.0
+        for j in range(tape.n_out):
+            g = got[out_off[j]:out_off[j + 1]].reshape(B, nout[j])[rows]
+            worst = max(worst, float(np.nanmax(np.abs(g - ref[j]) / np.maximum(np.abs(ref[j]), 1.0))))
+        info = plan.info
+        gbs = 8 * (sum(nin) + sum(nout)) * B / t / 1e9
+        out.append({"workload": name, "batch": B, "value": B / t, "unit": "evals/s", "ms_per_step": t * 1e3,
+                    "hbm_gbs": gbs, "hbm_frac": gbs / hbm_gbs, "team": info["team"], "n_chunks": info["n_chunks"],
+                    "max_rel_err_16_rows": worst})
+        del d_in, d_out
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -355,6 +412,7 @@ def run_ours(args):
                    (world * B * e2e_steps / e2e_s) / rate}
 
     ifetch = ifetch_roof(plan, info, B, mean_s, clocks)
+    secondary = secondary_points(dev, local, hbm_gbs) if (world == 1 and not args.no_secondary) else None
     traffic, traffic_src = committed_traffic(args.workload, info, B)
 
     line = {
@@ -389,6 +447,7 @@ def run_ours(args):
         "clocks": clocks,
         "parity": parity,
         "cpu_baseline": cpu,
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -416,6 +475,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-w1", action="store_true", help="also time the oracle with one thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the other-config points (cartpole/pendulum 1e6, humanoid/srbm 65536)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -819,8 +819,8 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             // reads a cross-warp value it has not yet synced for; otherwise it just *arrives*
             // (bar.arrive: release, no wait) and runs on into its next phase.  Ops of a phase
             // that need no fresh cross-warp value are hoisted ahead of those that do.
-            static const bool no_split = getenv("VSB_NO_SPLIT") != nullptr;
-            const bool split = K == 1 && !no_split && opt.split_barriers;
+            static const bool env_split = getenv("VSB_SPLIT") != nullptr;
+            const bool split = K == 1 && (opt.split_barriers || env_split);
             auto in_chunk0 = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
             auto xwarp = [&](int32_t u, int w) { return in_chunk0(u) && warp_of[u] != w; };
             if (split) {
@@ -960,8 +960,8 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             // occupies two slot rows laid out [row pair][lane][2]
             std::vector<int32_t> mate(N, -1);
             std::vector<uint8_t> second(N, 0);
-            static const bool no_pair = getenv("VSB_NO_PAIR") != nullptr;
-            const bool pairing = opt.pair_xfers && K == 1 && !no_pair;
+            static const bool env_pair = getenv("VSB_PAIR") != nullptr;
+            const bool pairing = (opt.pair_xfers || env_pair) && K == 1;
             if (pairing) {
                 std::map<std::vector<int32_t>, int32_t> open;  // signature -> unpaired value
                 for (int w = 0; w < W; ++w)
@@ -1021,7 +1021,12 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 ch.pairs = np;
             };
             allocate();
-            // over the smem budget (separate pair pool, or rows held back for split-barrier WAR
+            if (pairing && n_smem > cap) {  // separate pair pool fragmented past the budget: unpaired
+                std::fill(mate.begin(), mate.end(), -1);
+                std::fill(second.begin(), second.end(), 0);
+                allocate();
+            }
+            // still over the smem budget (separate pair pool, or rows held back for split-barrier WAR
             // safety): demote the longest-lived smem values to global scratch until it fits
             for (int iter = 0; n_smem > cap && iter < 64; ++iter) {
                 std::vector<int32_t> cand;

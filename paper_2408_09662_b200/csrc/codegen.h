@@ -83,8 +83,12 @@ struct EmitOptions {
     // subroutines (straight-line team code is instruction-fetch bound; one
     // resident copy of the division / trig sequence beats one per use)
     int outline = 0;
-    bool pair_xfers = true;    // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
-    bool split_barriers = true;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
+    // measured on srbm_mpc B=4096 (profiles/r1_sweeps_r15_r16.jsonl) and off by default:
+    // pairing saves 4% of the SASS but not time (0.412 vs 0.407 ms); split barriers let
+    // warps run ahead into their next phase but were slower (team 8: 0.485 vs 0.446 ms) --
+    // the early warps compete for the chip-wide instruction fetch with the critical ones
+    bool pair_xfers = false;   // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
+    bool split_barriers = false;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
 };
 
 struct Chunk {
