@@ -592,6 +592,13 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         hdr.s += "#define VS_CBAR() asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\")\n";
     if (trig_exact) {
         hdr.s += "#define VS_MATH_DEVICE 1\n";
+        // table-based fast path: fewer DP instructions but a dependent table load (latency);
+        // VSB_TRIG_FAST=0/1 overrides the per-mode default
+        {
+            static const char* tf = getenv("VSB_TRIG_FAST");
+            const bool fast = tf ? atoi(tf) != 0 : opt.trig_fast;
+            if (!fast) hdr.s += "#define VSM_NO_FAST 1\n";
+        }
         hdr.s += kVsMathSource;
         hdr.s += "\n";
     }

@@ -65,6 +65,7 @@ struct EmitOptions {
     int64_t chunk_ops = 0;     // target live ops per chunk kernel; 0 = auto
     int64_t smem_budget = 96 * 1024;  // bytes of static+dynamic smem for I/O staging
     bool exact_trig = true;    // f64 SIN/COS via vs_math.h (correctly rounded) instead of libdevice
+    bool trig_fast = true;     // vs_math.h table-based Ziv fast path before the double-double path
     // team mode: `team` warps share 32 instances (lane = instance); the DAG is
     // list-scheduled across warps in barrier-separated phases, cross-warp
     // values travel through shared memory.  0 = one thread per instance.

@@ -664,9 +664,11 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     const int rs = p->rsz();
     const int64_t n = e1 - e0;
     const int64_t row_bytes = (p->prog.in_base[n_in] + p->prog.out_base[n_out]) * rs;
-    // pieces: >= 4 MiB of I/O each, at most 8, so copies overlap the kernels
-    int64_t pieces = std::min<int64_t>(8, std::max<int64_t>(1, n * row_bytes / (4 << 20)));
-    const int64_t BS = 128;
+    // pieces: >= VSB_HOST_PIECE_BYTES (default 4 MiB) of I/O each, at most 8, so copies overlap
+    // the kernels; a piece is a whole number of CTAs (team kernels: 32 instances)
+    static const int64_t piece_bytes = getenv("VSB_HOST_PIECE_BYTES") ? atoll(getenv("VSB_HOST_PIECE_BYTES")) : (4 << 20);
+    int64_t pieces = std::min<int64_t>(8, std::max<int64_t>(1, n * row_bytes / std::max<int64_t>(piece_bytes, 1)));
+    const int64_t BS = v->ks.team >= 2 ? v->ks.chunks.front().inst_per_block : 128;
     int64_t piece = (n + pieces - 1) / pieces;
     piece = (piece + BS - 1) / BS * BS;
     cudaStream_t s0 = streams[0];

@@ -452,6 +452,12 @@ VSM_FN double vs_cos_slow(vsm_dd r, int q) {
     return ((q + 1) & 2) ? -c : c;
 }
 
+#ifdef VSM_NO_FAST
+#define VSM_TRY_FAST(r, s, c, w) 0
+#else
+#define VSM_TRY_FAST(r, s, c, w) vsm_fast_sc(r, s, c, w)
+#endif
+
 VSM_FN double vs_sin(double x) {
     double ax = x < 0.0 ? -x : x;
     if (!(ax < 1073741824.0)) return VSM_SIN_FALLBACK(x);   /* NaN, inf, |x| >= 2^30 */
@@ -459,7 +465,7 @@ VSM_FN double vs_sin(double x) {
     vsm_dd r;
     int q = (int)((long long)vsm_reduce(x, &r) & 3);
     double sv, cv;
-    if (vsm_fast_sc(r, &sv, &cv, (q & 1) ? 2 : 1)) {
+    if (VSM_TRY_FAST(r, &sv, &cv, (q & 1) ? 2 : 1)) {
         double v = (q & 1) ? cv : sv;
         return (q & 2) ? -v : v;
     }
@@ -473,7 +479,7 @@ VSM_FN double vs_cos(double x) {
     vsm_dd r;
     int q = (int)((long long)vsm_reduce(x, &r) & 3);
     double sv, cv;
-    if (vsm_fast_sc(r, &sv, &cv, (q & 1) ? 1 : 2)) {
+    if (VSM_TRY_FAST(r, &sv, &cv, (q & 1) ? 1 : 2)) {
         double v = (q & 1) ? sv : cv;
         return ((q + 1) & 2) ? -v : v;
     }
@@ -488,7 +494,7 @@ VSM_FN void vs_sincos(double x, double *s, double *c) {
     vsm_dd r;
     int q = (int)((long long)vsm_reduce(x, &r) & 3);
     double sv, cv;
-    if (!vsm_fast_sc(r, &sv, &cv, 3)) {
+    if (!VSM_TRY_FAST(r, &sv, &cv, 3)) {
         vsm_dd vs = vsm_sin_kernel(r), vc = vsm_cos_kernel(r);
         sv = vs.hi + vs.lo;
         cv = vc.hi + vc.lo;
