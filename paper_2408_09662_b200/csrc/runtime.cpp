@@ -249,6 +249,10 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
     eo.smem_budget = p->opts.smem_budget;
     eo.exact_trig = p->opts.libdevice_trig == 0;
+    // the table-based sin/cos fast path trades DP instructions for a dependent table load:
+    // a win for thread-per-instance kernels, a loss on the team kernels' critical path
+    // (humanoid_rbd B=65536: 1.06 vs 0.77 ms; profiles/r1_sweeps_r19.jsonl)
+    eo.trig_fast = p->opts.team < 2;
     eo.team = p->opts.team;
     eo.phase_cost = p->opts.phase_cost;
     eo.priority = p->opts.priority;
@@ -451,7 +455,8 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     if (p->opts.dtype != VSB_F64 && p->opts.dtype != VSB_F32) return fail(VSB_ERR_INVALID, "unknown dtype");
     if (p->opts.block <= 0) p->opts.block = 128;
     if (p->opts.block % 32 != 0 || p->opts.block > 1024) return fail(VSB_ERR_INVALID, "block must be a multiple of 32 in [32, 1024]");
-    if (p->opts.min_blocks <= 0) p->opts.min_blocks = 1;
+    const bool auto_min_blocks = p->opts.min_blocks <= 0;
+    if (auto_min_blocks) p->opts.min_blocks = 1;
     if (p->opts.smem_budget <= 0) p->opts.smem_budget = 96 * 1024;
     if (p->opts.team < 0 || p->opts.team > 32) return fail(VSB_ERR_INVALID, "team must be in [0, 32]");
     if (p->opts.phase_cost <= 0) p->opts.phase_cost = 96;
@@ -468,6 +473,11 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     // (srbm_mpc 111k ops, B=4096, outlined DIV, profiles/r1_sweeps_r12.jsonl: team 16 / 12 = 0.402 / 0.418 ms)
     if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 40000 ? 16 : p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
+    // thread mode, small tapes: 8 CTAs of 128 per SM (64 registers) hide the latency of the
+    // per-thread dependency chains (cartpole_rk4 B=1e6: 0.096 -> 0.076 ms, pendulum 0.041 ->
+    // 0.033 ms; profiles/r1_sweeps_r19.jsonl)
+    if (auto_min_blocks && p->opts.team == 0 && p->opts.block == 128 && p->prog.n_live_ops <= 600)
+        p->opts.min_blocks = 8;
     if (p->opts.groups < 0 || p->opts.groups > 32) return fail(VSB_ERR_INVALID, "groups must be in [0, 32]");
     if (p->opts.cluster < 0 || p->opts.cluster > 16) return fail(VSB_ERR_INVALID, "cluster must be in [0, 16]");
     if (p->opts.groups == 0) p->opts.groups = 1;
