@@ -655,15 +655,16 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
     CUDA_TRY(cudaSetDevice(device));
+    constexpr int kMaxPieces = 8;
     Variant* v;
-    std::vector<cudaStream_t> streams;
+    std::vector<cudaStream_t> streams;  // [0] H2D, [1] D2H, [2..] one compute stream per piece
     {
         std::lock_guard<std::mutex> lk(p->mu);
         rc = build_variant(p, VSB_AOS, &v);
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
         if (rc != VSB_OK) return rc;
         auto& ss = p->streams[device];
-        while (ss.size() < 3) {
+        while (ss.size() < 2 + kMaxPieces) {
             cudaStream_t s;
             CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
             ss.push_back(s);
@@ -674,60 +675,76 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     const int rs = p->rsz();
     const int64_t n = e1 - e0;
     const int64_t row_bytes = (p->prog.in_base[n_in] + p->prog.out_base[n_out]) * rs;
-    // pieces: >= VSB_HOST_PIECE_BYTES (default 4 MiB) of I/O each, at most 8, so copies overlap
-    // the kernels; a piece is a whole number of CTAs (team kernels: 32 instances)
+    // pipeline: all H2D copies in order on one copy stream, each piece's kernel chain on its
+    // own stream as soon as its inputs landed, D2H in piece order on a second copy stream.
+    // Pieces: >= VSB_HOST_PIECE_BYTES of I/O (default 4 MiB), <= 8, whole CTAs.  Team kernels
+    // are latency-bound (a piece's chain takes about as long as the whole batch's), so early
+    // pieces start computing while later inputs are still in flight.
     static const int64_t piece_bytes = getenv("VSB_HOST_PIECE_BYTES") ? atoll(getenv("VSB_HOST_PIECE_BYTES")) : (4 << 20);
-    int64_t pieces = std::min<int64_t>(8, std::max<int64_t>(1, n * row_bytes / std::max<int64_t>(piece_bytes, 1)));
+    int64_t pieces = std::min<int64_t>(kMaxPieces, std::max<int64_t>(1, n * row_bytes / std::max<int64_t>(piece_bytes, 1)));
     const int64_t BS = v->ks.team >= 2 ? v->ks.chunks.front().inst_per_block : 128;
     int64_t piece = (n + pieces - 1) / pieces;
     piece = (piece + BS - 1) / BS * BS;
-    cudaStream_t s0 = streams[0];
+    pieces = (n + piece - 1) / piece;
+    cudaStream_t sh = streams[0], sd = streams[1];
     std::vector<void*> d_in(n_in, nullptr), d_out(n_out, nullptr);
     for (int i = 0; i < n_in; ++i)
-        if (p->prog.nnz_in[i]) CUDA_TRY(cudaMallocAsync(&d_in[i], static_cast<size_t>(n * p->prog.nnz_in[i] * rs), s0));
+        if (p->prog.nnz_in[i]) CUDA_TRY(cudaMallocAsync(&d_in[i], static_cast<size_t>(n * p->prog.nnz_in[i] * rs), sh));
     for (int j = 0; j < n_out; ++j)
-        if (p->prog.nnz_out[j]) CUDA_TRY(cudaMallocAsync(&d_out[j], static_cast<size_t>(n * p->prog.nnz_out[j] * rs), s0));
-    cudaEvent_t ready;
-    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    cudaEventRecord(ready, s0);
-    for (auto s : streams) cudaStreamWaitEvent(s, ready, 0);
+        if (p->prog.nnz_out[j]) CUDA_TRY(cudaMallocAsync(&d_out[j], static_cast<size_t>(n * p->prog.nnz_out[j] * rs), sh));
+    std::vector<cudaEvent_t> ev(2 * pieces + 1);
+    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t alloc_done = ev[2 * pieces];
+    cudaEventRecord(alloc_done, sh);
+    cudaStreamWaitEvent(sd, alloc_done, 0);
     const char* hin = static_cast<const char*>(in_buf);
     char* hout = static_cast<char*>(out_buf);
-    int k = 0;
-    for (int64_t lo = 0; lo < n && rc == VSB_OK; lo += piece, ++k) {
-        const int64_t hi = std::min(n, lo + piece), m = hi - lo;
-        cudaStream_t s = streams[k % streams.size()];
-        std::vector<const void*> ins(n_in);
-        std::vector<void*> outs(n_out);
+    // 1. H2D of every piece, in order
+    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
+        const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         for (int i = 0; i < n_in; ++i) {
             const int64_t nz = p->prog.nnz_in[i];
-            ins[i] = d_in[i];
             if (!nz) continue;
             cudaError_t e = cudaMemcpyAsync(static_cast<char*>(d_in[i]) + lo * nz * rs,
                                             hin + (in_off[i] + (e0 + lo) * nz) * rs, static_cast<size_t>(m * nz * rs),
-                                            cudaMemcpyHostToDevice, s);
+                                            cudaMemcpyHostToDevice, sh);
             if (e != cudaSuccess) { rc = fail(VSB_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e)); break; }
         }
-        for (int j = 0; j < n_out; ++j) outs[j] = d_out[j];
-        if (rc == VSB_OK) rc = launch_chain(p, v, ins, outs, lo, m, 0, s, device);
+        cudaEventRecord(ev[k], sh);
+    }
+    // 2. kernels per piece on their own stream
+    std::vector<const void*> ins(n_in);
+    std::vector<void*> outs(n_out);
+    for (int i = 0; i < n_in; ++i) ins[i] = d_in[i];
+    for (int j = 0; j < n_out; ++j) outs[j] = d_out[j];
+    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
+        const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
+        cudaStream_t sc = streams[2 + k];
+        cudaStreamWaitEvent(sc, ev[k], 0);
+        rc = launch_chain(p, v, ins, outs, lo, m, 0, sc, device);
+        cudaEventRecord(ev[pieces + k], sc);
+    }
+    // 3. D2H in piece order
+    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
+        const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
+        cudaStreamWaitEvent(sd, ev[pieces + k], 0);
         for (int j = 0; j < n_out && rc == VSB_OK; ++j) {
             const int64_t nz = p->prog.nnz_out[j];
             if (!nz) continue;
             cudaError_t e = cudaMemcpyAsync(hout + (out_off[j] + (e0 + lo) * nz) * rs,
                                             static_cast<char*>(d_out[j]) + lo * nz * rs, static_cast<size_t>(m * nz * rs),
-                                            cudaMemcpyDeviceToHost, s);
+                                            cudaMemcpyDeviceToHost, sd);
             if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
         }
     }
-    // join all streams back on s0 before freeing
-    for (size_t q = 1; q < streams.size(); ++q) {
-        cudaEventRecord(ready, streams[q]);
-        cudaStreamWaitEvent(s0, ready, 0);
-    }
-    for (auto ptr : d_in) if (ptr) cudaFreeAsync(ptr, s0);
-    for (auto ptr : d_out) if (ptr) cudaFreeAsync(ptr, s0);
-    cudaError_t e = cudaStreamSynchronize(s0);
-    cudaEventDestroy(ready);
+    // join the compute streams (already ordered before the D2H) and the copy streams, then free
+    for (int64_t k = 0; k < pieces; ++k) cudaStreamWaitEvent(sd, ev[pieces + k], 0);
+    cudaEventRecord(alloc_done, sh);
+    cudaStreamWaitEvent(sd, alloc_done, 0);
+    for (auto ptr : d_in) if (ptr) cudaFreeAsync(ptr, sd);
+    for (auto ptr : d_out) if (ptr) cudaFreeAsync(ptr, sd);
+    cudaError_t e = cudaStreamSynchronize(sd);
+    for (auto x : ev) cudaEventDestroy(x);
     if (rc != VSB_OK) return rc;
     if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("eval_host: ") + cudaGetErrorString(e));
     return VSB_OK;
