@@ -227,6 +227,10 @@ struct vsb_plan {
     std::mutex mu;
     std::map<int, std::unique_ptr<Variant>> variants;  // by layout
     std::map<int, std::vector<cudaStream_t>> streams;  // host-pipeline streams per device
+    // persistent device workspace of the host path (inputs, outputs, per-piece scratch), per
+    // device, grow-only: no stream-ordered pool traffic between the pipeline's streams
+    struct HostWs { void* base = nullptr; size_t bytes = 0; std::unique_ptr<std::mutex> mu{new std::mutex}; };
+    std::map<int, HostWs> host_ws;
     std::set<int> pool_ready;
     std::string last_log;
     int rsz() const { return opts.dtype == VSB_F32 ? 4 : 8; }
@@ -371,8 +375,20 @@ int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
 }
 
 // launch the kernel chain for elements [e0, e0+n) (indices relative to in/out pointers)
+// bytes of SoA scratch a launch_chain over n instances needs (0 if none)
+int64_t chain_scratch_bytes(vsb_plan* p, Variant* v, int64_t n, int n_sm) {
+    if (n <= 0 || v->ks.scratch_slots == 0) return 0;
+    int ipb_max = 32;
+    for (auto& ch : v->ks.chunks) ipb_max = std::max(ipb_max, ch.inst_per_block);
+    const int64_t wave = auto_wave(p, v, n);
+    auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
+    const int64_t units = std::max(units_of(wave), units_of(n % wave));
+    const int64_t ld_max = std::max<int64_t>((wave + ipb_max - 1) / ipb_max, units) * ipb_max;
+    return ld_max * v->ks.scratch_slots * p->rsz();
+}
+
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
-                 int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device) {
+                 int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device, void* scratch_pre = nullptr) {
     if (n <= 0) return VSB_OK;
     int ipb_max = 32;
     for (auto& ch : v->ks.chunks) ipb_max = std::max(ipb_max, ch.inst_per_block);
@@ -384,10 +400,11 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     // every chunk of a variant has the same shape; scratch holds VS_IPB rows per cluster
     // (or block) of the biggest launch: a full wave or the remainder wave
     auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
-    void* scratch = nullptr;
+    void* scratch = scratch_pre;
     const int64_t units = std::max(units_of(wave), units_of(n % wave));
     const int64_t ld_max = std::max<int64_t>((wave + BS - 1) / BS, units) * BS;
-    if (v->ks.scratch_slots > 0) {
+    const bool own_scratch = v->ks.scratch_slots > 0 && !scratch_pre;
+    if (own_scratch) {
         ensure_pool(p, device);
         CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(ld_max * v->ks.scratch_slots * p->rsz()), stream));
     }
@@ -417,7 +434,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             }
         }
     }
-    if (scratch) cudaFreeAsync(scratch, stream);
+    if (own_scratch) cudaFreeAsync(scratch, stream);
     return rc;
 }
 
@@ -497,6 +514,14 @@ int vsb_plan_destroy(vsb_plan* p) {
     if (!p) return VSB_OK;
     for (auto& kv : p->variants)
         for (auto lib : kv.second->libs) cudaLibraryUnload(lib);
+    for (auto& kv : p->host_ws) {
+        if (!kv.second.base) continue;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second.base);
+        cudaSetDevice(prev);
+    }
     for (auto& kv : p->streams) {
         int prev = 0;
         cudaGetDevice(&prev);
@@ -687,11 +712,35 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     piece = (piece + BS - 1) / BS * BS;
     pieces = (n + piece - 1) / piece;
     cudaStream_t sh = streams[0], sd = streams[1];
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    // carve the persistent workspace: inputs, outputs, scratch per piece (256-byte aligned)
+    auto align = [](int64_t b) { return (b + 255) / 256 * 256; };
+    std::vector<int64_t> off_in(n_in), off_out(n_out), off_scr(pieces);
+    int64_t total = 0;
+    for (int i = 0; i < n_in; ++i) { off_in[i] = total; total += align(n * p->prog.nnz_in[i] * rs); }
+    for (int j = 0; j < n_out; ++j) { off_out[j] = total; total += align(n * p->prog.nnz_out[j] * rs); }
+    for (int64_t k = 0; k < pieces; ++k) {
+        off_scr[k] = total;
+        total += align(chain_scratch_bytes(p, v, std::min(n, (k + 1) * piece) - k * piece, n_sm));
+    }
+    vsb_plan::HostWs* ws;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        ws = &p->host_ws[device];
+    }
+    std::lock_guard<std::mutex> ws_lock(*ws->mu);  // one host-path call per device at a time
+    if (ws->bytes < static_cast<size_t>(total)) {
+        if (ws->base) CUDA_TRY(cudaFree(ws->base));
+        ws->base = nullptr;
+        ws->bytes = 0;
+        CUDA_TRY(cudaMalloc(&ws->base, static_cast<size_t>(std::max<int64_t>(total, 256))));
+        ws->bytes = static_cast<size_t>(std::max<int64_t>(total, 256));
+    }
+    char* wb = static_cast<char*>(ws->base);
     std::vector<void*> d_in(n_in, nullptr), d_out(n_out, nullptr);
-    for (int i = 0; i < n_in; ++i)
-        if (p->prog.nnz_in[i]) CUDA_TRY(cudaMallocAsync(&d_in[i], static_cast<size_t>(n * p->prog.nnz_in[i] * rs), sh));
-    for (int j = 0; j < n_out; ++j)
-        if (p->prog.nnz_out[j]) CUDA_TRY(cudaMallocAsync(&d_out[j], static_cast<size_t>(n * p->prog.nnz_out[j] * rs), sh));
+    for (int i = 0; i < n_in; ++i) if (p->prog.nnz_in[i]) d_in[i] = wb + off_in[i];
+    for (int j = 0; j < n_out; ++j) if (p->prog.nnz_out[j]) d_out[j] = wb + off_out[j];
     std::vector<cudaEvent_t> ev(2 * pieces + 1);
     for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaEvent_t alloc_done = ev[2 * pieces];
@@ -721,7 +770,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         cudaStream_t sc = streams[2 + k];
         cudaStreamWaitEvent(sc, ev[k], 0);
-        rc = launch_chain(p, v, ins, outs, lo, m, 0, sc, device);
+        rc = launch_chain(p, v, ins, outs, lo, m, 0, sc, device, v->ks.scratch_slots > 0 ? wb + off_scr[k] : nullptr);
         cudaEventRecord(ev[pieces + k], sc);
     }
     // 3. D2H in piece order
@@ -741,8 +790,6 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     for (int64_t k = 0; k < pieces; ++k) cudaStreamWaitEvent(sd, ev[pieces + k], 0);
     cudaEventRecord(alloc_done, sh);
     cudaStreamWaitEvent(sd, alloc_done, 0);
-    for (auto ptr : d_in) if (ptr) cudaFreeAsync(ptr, sd);
-    for (auto ptr : d_out) if (ptr) cudaFreeAsync(ptr, sd);
     cudaError_t e = cudaStreamSynchronize(sd);
     for (auto x : ev) cudaEventDestroy(x);
     if (rc != VSB_OK) return rc;
