@@ -707,6 +707,10 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     // pieces start computing while later inputs are still in flight.
     static const int64_t piece_bytes = getenv("VSB_HOST_PIECE_BYTES") ? atoll(getenv("VSB_HOST_PIECE_BYTES")) : (4 << 20);
     int64_t pieces = std::min<int64_t>(kMaxPieces, std::max<int64_t>(1, n * row_bytes / std::max<int64_t>(piece_bytes, 1)));
+    // team kernels are latency-bound: a piece's chain takes nearly as long as the whole
+    // batch's, so splitting only adds copies (srbm_mpc B=4096, VSB_TRACE: 1 piece 0.72 ms,
+    // 3 pieces 0.75, 8 pieces 0.81)
+    if (v->ks.team >= 2 && !getenv("VSB_HOST_PIECE_BYTES")) pieces = 1;
     const int64_t BS = v->ks.team >= 2 ? v->ks.chunks.front().inst_per_block : 128;
     int64_t piece = (n + pieces - 1) / pieces;
     piece = (piece + BS - 1) / BS * BS;
@@ -718,8 +722,12 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     auto align = [](int64_t b) { return (b + 255) / 256 * 256; };
     std::vector<int64_t> off_in(n_in), off_out(n_out), off_scr(pieces);
     int64_t total = 0;
-    for (int i = 0; i < n_in; ++i) { off_in[i] = total; total += align(n * p->prog.nnz_in[i] * rs); }
-    for (int j = 0; j < n_out; ++j) { off_out[j] = total; total += align(n * p->prog.nnz_out[j] * rs); }
+    // inputs back to back, outputs back to back (same relative layout as a full-range
+    // BatchWorkspace, so one copy can move all of them)
+    for (int i = 0; i < n_in; ++i) { off_in[i] = total; total += n * p->prog.nnz_in[i] * rs; }
+    total = align(total);
+    for (int j = 0; j < n_out; ++j) { off_out[j] = total; total += n * p->prog.nnz_out[j] * rs; }
+    total = align(total);
     for (int64_t k = 0; k < pieces; ++k) {
         off_scr[k] = total;
         total += align(chain_scratch_bytes(p, v, std::min(n, (k + 1) * piece) - k * piece, n_sm));
@@ -741,15 +749,36 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     std::vector<void*> d_in(n_in, nullptr), d_out(n_out, nullptr);
     for (int i = 0; i < n_in; ++i) if (p->prog.nnz_in[i]) d_in[i] = wb + off_in[i];
     for (int j = 0; j < n_out; ++j) if (p->prog.nnz_out[j]) d_out[j] = wb + off_out[j];
+    static const bool trace = getenv("VSB_TRACE") != nullptr;
     std::vector<cudaEvent_t> ev(2 * pieces + 1);
-    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+    std::vector<cudaEvent_t> tev;  // VSB_TRACE: t0, kernel start per piece, D2H done
+    if (trace) {
+        tev.resize(pieces + 2);
+        for (auto& e : tev) cudaEventCreate(&e);
+        cudaEventRecord(tev[0], sh);
+    }
     cudaEvent_t alloc_done = ev[2 * pieces];
     cudaEventRecord(alloc_done, sh);
     cudaStreamWaitEvent(sd, alloc_done, 0);
     const char* hin = static_cast<const char*>(in_buf);
     char* hout = static_cast<char*>(out_buf);
+    // host regions of consecutive inputs (outputs) abut: move them with one copy
+    auto contiguous = [&](const int64_t* off, const std::vector<int64_t>& nnz) {
+        for (size_t i = 0; i + 1 < nnz.size(); ++i)
+            if (off[i] + (e0 + n) * nnz[i] != off[i + 1] + e0 * nnz[i + 1]) return false;
+        return true;
+    };
+    const bool one_in = pieces == 1 && n_in > 0 && contiguous(in_off, p->prog.nnz_in);
+    const bool one_out = pieces == 1 && n_out > 0 && contiguous(out_off, p->prog.nnz_out);
+    if (one_in && p->prog.in_base[n_in] > 0) {
+        cudaError_t e = cudaMemcpyAsync(wb + off_in[0], hin + (in_off[0] + e0 * p->prog.nnz_in[0]) * rs,
+                                        static_cast<size_t>(n * p->prog.in_base[n_in] * rs), cudaMemcpyHostToDevice, sh);
+        if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
+        cudaEventRecord(ev[0], sh);
+    }
     // 1. H2D of every piece, in order
-    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
+    for (int64_t k = 0; k < pieces && rc == VSB_OK && !one_in; ++k) {
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         for (int i = 0; i < n_in; ++i) {
             const int64_t nz = p->prog.nnz_in[i];
@@ -770,11 +799,18 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         cudaStream_t sc = streams[2 + k];
         cudaStreamWaitEvent(sc, ev[k], 0);
+        if (trace) cudaEventRecord(tev[1 + k], sc);
         rc = launch_chain(p, v, ins, outs, lo, m, 0, sc, device, v->ks.scratch_slots > 0 ? wb + off_scr[k] : nullptr);
         cudaEventRecord(ev[pieces + k], sc);
     }
+    if (one_out && rc == VSB_OK && p->prog.out_base[n_out] > 0) {
+        cudaStreamWaitEvent(sd, ev[pieces], 0);
+        cudaError_t e = cudaMemcpyAsync(hout + (out_off[0] + e0 * p->prog.nnz_out[0]) * rs, wb + off_out[0],
+                                        static_cast<size_t>(n * p->prog.out_base[n_out] * rs), cudaMemcpyDeviceToHost, sd);
+        if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
+    }
     // 3. D2H in piece order
-    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
+    for (int64_t k = 0; k < pieces && rc == VSB_OK && !one_out; ++k) {
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         cudaStreamWaitEvent(sd, ev[pieces + k], 0);
         for (int j = 0; j < n_out && rc == VSB_OK; ++j) {
@@ -790,7 +826,17 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     for (int64_t k = 0; k < pieces; ++k) cudaStreamWaitEvent(sd, ev[pieces + k], 0);
     cudaEventRecord(alloc_done, sh);
     cudaStreamWaitEvent(sd, alloc_done, 0);
+    if (trace) cudaEventRecord(tev[pieces + 1], sd);
     cudaError_t e = cudaStreamSynchronize(sd);
+    if (trace) {
+        auto ms = [&](cudaEvent_t a, cudaEvent_t b) { float t = 0; cudaEventElapsedTime(&t, a, b); return t; };
+        fprintf(stderr, "[vsb trace] n=%lld pieces=%lld:", (long long)n, (long long)pieces);
+        for (int64_t k = 0; k < pieces; ++k)
+            fprintf(stderr, " p%lld h2d %.3f kstart %.3f kdone %.3f |", (long long)k, ms(tev[0], ev[k]), ms(tev[0], tev[1 + k]),
+                    ms(tev[0], ev[pieces + k]));
+        fprintf(stderr, " end %.3f ms\n", ms(tev[0], tev[pieces + 1]));
+        for (auto x : tev) cudaEventDestroy(x);
+    }
     for (auto x : ev) cudaEventDestroy(x);
     if (rc != VSB_OK) return rc;
     if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("eval_host: ") + cudaGetErrorString(e));
