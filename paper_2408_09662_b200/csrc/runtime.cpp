@@ -229,7 +229,13 @@ struct vsb_plan {
     std::map<int, std::vector<cudaStream_t>> streams;  // host-pipeline streams per device
     // persistent device workspace of the host path (inputs, outputs, per-piece scratch), per
     // device, grow-only: no stream-ordered pool traffic between the pipeline's streams
-    struct HostWs { void* base = nullptr; size_t bytes = 0; std::unique_ptr<std::mutex> mu{new std::mutex}; };
+    struct HostWs {
+        void* base = nullptr;
+        size_t bytes = 0;
+        std::unique_ptr<std::mutex> mu{new std::mutex};
+        std::vector<cudaEvent_t> events;   // reused across calls (guarded by mu)
+        int n_sm = 0;
+    };
     std::map<int, HostWs> host_ws;
     std::set<int> pool_ready;
     std::string last_log;
@@ -354,6 +360,19 @@ int64_t auto_wave(vsb_plan* p, const Variant* v, int64_t n) {
     return std::min(n, w);
 }
 
+// SM count per device (queried once)
+int sm_count(int device) {
+    static std::atomic<int> cache[64];
+    if (device < 0 || device >= 64) return 148;
+    int n = cache[device].load(std::memory_order_relaxed);
+    if (n == 0) {
+        n = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        cache[device].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
 // instances per cluster for a launch of m instances: team kernels take up to
 // `ipb` per cluster; optionally (VSB_IPC_FILL=1), when the grid would leave SMs
 // idle in its last wave, fewer instances per cluster (spare lanes idle) give the
@@ -395,8 +414,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     const int BS = ipb_max;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     const int64_t wave = auto_wave(p, v, n);
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    const int n_sm = sm_count(device);
     // every chunk of a variant has the same shape; scratch holds VS_IPB rows per cluster
     // (or block) of the biggest launch: a full wave or the remainder wave
     auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
@@ -515,11 +533,11 @@ int vsb_plan_destroy(vsb_plan* p) {
     for (auto& kv : p->variants)
         for (auto lib : kv.second->libs) cudaLibraryUnload(lib);
     for (auto& kv : p->host_ws) {
-        if (!kv.second.base) continue;
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(kv.first);
-        cudaFree(kv.second.base);
+        if (kv.second.base) cudaFree(kv.second.base);
+        for (auto e : kv.second.events) cudaEventDestroy(e);
         cudaSetDevice(prev);
     }
     for (auto& kv : p->streams) {
@@ -716,8 +734,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     piece = (piece + BS - 1) / BS * BS;
     pieces = (n + piece - 1) / piece;
     cudaStream_t sh = streams[0], sd = streams[1];
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    const int n_sm = sm_count(device);
     // carve the persistent workspace: inputs, outputs, scratch per piece (256-byte aligned)
     auto align = [](int64_t b) { return (b + 255) / 256 * 256; };
     std::vector<int64_t> off_in(n_in), off_out(n_out), off_scr(pieces);
@@ -750,8 +767,12 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     for (int i = 0; i < n_in; ++i) if (p->prog.nnz_in[i]) d_in[i] = wb + off_in[i];
     for (int j = 0; j < n_out; ++j) if (p->prog.nnz_out[j]) d_out[j] = wb + off_out[j];
     static const bool trace = getenv("VSB_TRACE") != nullptr;
-    std::vector<cudaEvent_t> ev(2 * pieces + 1);
-    for (auto& e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+    while (ws->events.size() < static_cast<size_t>(2 * pieces + 1)) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+        ws->events.push_back(e);
+    }
+    std::vector<cudaEvent_t> ev(ws->events.begin(), ws->events.begin() + (2 * pieces + 1));
     std::vector<cudaEvent_t> tev;  // VSB_TRACE: t0, kernel start per piece, D2H done
     if (trace) {
         tev.resize(pieces + 2);
@@ -837,7 +858,6 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         fprintf(stderr, " end %.3f ms\n", ms(tev[0], tev[pieces + 1]));
         for (auto x : tev) cudaEventDestroy(x);
     }
-    for (auto x : ev) cudaEventDestroy(x);
     if (rc != VSB_OK) return rc;
     if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("eval_host: ") + cudaGetErrorString(e));
     return VSB_OK;
