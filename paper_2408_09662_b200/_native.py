@@ -59,6 +59,7 @@ class Options(ctypes.Structure):
         ("groups", ctypes.c_int32),
         ("cluster", ctypes.c_int32),
         ("outline", ctypes.c_int32),
+        ("bulk_io", ctypes.c_int32),
     ]
 
 

@@ -264,6 +264,32 @@ __device__ __forceinline__ void vs_stage_out(real* __restrict__ g, const real* _
         }
     }
 }
+// ---- TMA bulk copies + mbarriers (persistent thread-mode kernels) ----
+__device__ __forceinline__ unsigned vs_sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void vs_mbar_init(unsigned long long* m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(vs_sa(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void vs_mbar_expect(unsigned long long* m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(vs_sa(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void vs_mbar_wait(unsigned long long* m, unsigned parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "VS_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra VS_WAIT_%=;\n}" :: "r"(vs_sa(m)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void vs_bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(vs_sa(dst)), "l"(src), "r"(bytes), "r"(vs_sa(m)) : "memory");
+}
+__device__ __forceinline__ void vs_bulk_store(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" :: "l"(dst), "r"(vs_sa(src)), "r"(bytes) : "memory");
+}
+#define VS_BULK_COMMIT() asm volatile("cp.async.bulk.commit_group;" ::: "memory")
+#define VS_BULK_WAIT_READ1() asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory")
+#define VS_BULK_WAIT_ALL() asm volatile("cp.async.bulk.wait_group 0;" ::: "memory")
+#define VS_FENCE_ASYNC() asm volatile("fence.proxy.async.shared::cta;" ::: "memory")
+#define VS_FENCE_MBAR_INIT() asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory")
 // FMIN/FMAX: NaN loses, ties keep the first operand (_kernels.py:116-143) -- explicit
 // selects, not DMNMX, so signed-zero ties match the reference bit for bit
 __device__ __forceinline__ real vs_fmin(real x, real y) { return (x != x) ? y : (y != y) ? x : (x <= y) ? x : y; }
@@ -809,6 +835,93 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 }
             }
             b.put("}\n");
+            // ---- persistent TMA variant: full 128-instance tiles stream through two smem
+            // buffers with cp.async.bulk (one bulk copy per input / output array, completion on
+            // an mbarrier), the next tiles' loads in flight while the current tile computes
+            const bool tma = opt.bulk_io && same_kernel && !soa && ni_tot > 0 && no_tot > 0 &&
+                             2 * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
+            if (tma) {
+                ch.tma = true;
+                const int64_t IT = ni_tot * opt.block, OT = no_tot * opt.block;  // tile sizes (elements)
+                ch.tma_smem_bytes = 2 * (IT + OT) * rsz + 16;
+                b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_tma(const VsArgs A) {\n", opt.min_blocks, nbuf);
+                b.put("    extern __shared__ __align__(128) real vs_smem[];\n");
+                b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", 2 * (IT + OT));
+                b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the runtime launches the tail separately\n");
+                b.put("    if (threadIdx.x == 0) { vs_mbar_init(mbar, 1); vs_mbar_init(mbar + 1, 1); VS_FENCE_MBAR_INIT(); }\n");
+                b.put("    __syncthreads();\n");
+                // loads of one tile into buffer bs
+                Out ld;
+                ld.put("    auto issue = [&](long long tile, int bs) {\n");
+                ld.put("        real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
+                ld.put("        const long long e = A.e0 + tile * VS_BS;\n");
+                ld.put("        vs_mbar_expect(mbar + bs, %" PRId64 "u);\n", IT * rsz);
+                for (int i = 0; i < n_in; ++i) {
+                    if (p.nnz_in[i] == 0) continue;
+                    ld.put("        vs_bulk_load(ib + %" PRId64 ", A.in[%d] + e * %" PRId64 "LL, %" PRId64 "u, mbar + bs);\n",
+                           p.in_base[i] * opt.block, i, p.nnz_in[i], p.nnz_in[i] * opt.block * rsz);
+                }
+                ld.put("    };\n");
+                b.s += ld.s;
+                b.put("    long long tile = blockIdx.x;\n");
+                b.put("    if (threadIdx.x == 0) {\n");
+                b.put("        if (tile < ntiles) issue(tile, 0);\n");
+                b.put("        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);\n");
+                b.put("    }\n");
+                b.put("    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {\n");
+                b.put("        const int bs = k & 1;\n");
+                b.put("        vs_mbar_wait(mbar + bs, (k >> 1) & 1);\n");
+                b.put("        if (threadIdx.x == 0 && k >= 2) VS_BULK_WAIT_READ1();  // out buffer bs free again\n");
+                b.put("        __syncthreads();\n");
+                b.put("        const real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
+                b.put("        real* ob = vs_smem + %" PRId64 " + bs * %" PRId64 ";\n", 2 * IT, OT);
+                for (int i = 0; i < n_in; ++i)
+                    b.put("        const real* __restrict__ I%d = ib + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", i,
+                          p.in_base[i] * opt.block, p.nnz_in[i]);
+                for (int j = 0; j < n_out; ++j)
+                    b.put("        real* __restrict__ O%d = ob + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", j,
+                          p.out_base[j] * opt.block, p.nnz_out[j]);
+                for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
+                for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
+                // body: same op sequence, inputs from the smem tile row, outputs to the smem out row
+                std::vector<uint8_t> done2(N, 0), got(N, 0);
+                const char* ind2 = "        ";
+                auto ensure2 = [&](int32_t u) {
+                    const Node& nu = p.nodes[u];
+                    if (nu.op != OP_INPUT || got[u]) return;
+                    got[u] = 1;
+                    b.put("%sconst real v%d = I%d[%d];\n", ind2, u, nu.in_i, nu.in_k);
+                };
+                for (size_t si = 0; si < p.stores.size(); ++si) {
+                    const int32_t u = p.stores[si].node;
+                    if (p.nodes[u].op > OP_INPUT) continue;
+                    ensure2(u);
+                    b.put("%sO%d[%d] = %s;\n", ind2, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
+                }
+                for (int64_t q = ch.first; q < ch.last; ++q) {
+                    const Node& nd = p.nodes[q];
+                    if (nd.op <= OP_ASSIGN) continue;
+                    for (int k = 0; k < kArity[nd.op]; ++k) ensure2(nd.arg[k]);
+                    emit_def(b, q, done2, ind2);
+                    for (int32_t si : stores_of[q])
+                        b.put("%sO%d[%d] = v%" PRId64 ";\n", ind2, p.stores[si].j, p.stores[si].k, q);
+                }
+                b.put("        VS_FENCE_ASYNC();   // generic-proxy smem writes -> visible to the bulk store\n");
+                b.put("        __syncthreads();\n");
+                b.put("        if (threadIdx.x == 0) {\n");
+                b.put("            const long long e = A.e0 + tile * VS_BS;\n");
+                for (int j = 0; j < n_out; ++j) {
+                    if (p.nnz_out[j] == 0) continue;
+                    b.put("            vs_bulk_store(A.out[%d] + e * %" PRId64 "LL, ob + %" PRId64 ", %" PRId64 "u);\n", j,
+                          p.nnz_out[j], p.out_base[j] * opt.block, p.nnz_out[j] * opt.block * rsz);
+                }
+                b.put("            VS_BULK_COMMIT();\n");
+                b.put("            if (tile + 2 * (long long)gridDim.x < ntiles) issue(tile + 2 * (long long)gridDim.x, bs);\n");
+                b.put("        }\n");
+                b.put("    }\n");
+                b.put("    if (threadIdx.x == 0) VS_BULK_WAIT_ALL();\n");
+                b.put("}\n");
+            }
         } else {
             // ================= team mode: W warps x 32 instances =================
             const int W = opt.team, K = TK, G = TG, Wl = TWl;

@@ -90,6 +90,7 @@ struct EmitOptions {
     // the early warps compete for the chip-wide instruction fetch with the critical ones
     bool pair_xfers = false;   // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
     bool split_barriers = false;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
+    bool bulk_io = true;       // thread mode, single kernel: also emit a persistent TMA (cp.async.bulk) variant
 };
 
 struct Chunk {
@@ -101,6 +102,8 @@ struct Chunk {
     int threads = 128;             // CTA size
     int inst_per_block = 128;      // instances per CTA (cluster in team mode: 32 * groups)
     int cluster = 1;               // CTAs per cluster (grid = clusters * cluster)
+    bool tma = false;              // the source also holds `<name>_tma` (persistent bulk-copy variant)
+    int64_t tma_smem_bytes = 0;
     // team-mode schedule statistics
     int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0, remote_stores = 0, pairs = 0;
     double est_efficiency = 0.0;   // total cost / (warps * sum of per-phase max load)

@@ -211,6 +211,8 @@ struct Variant {
     std::vector<CompiledChunk> compiled;
     std::vector<cudaLibrary_t> libs;     // loaded lazily (context-independent)
     std::vector<cudaKernel_t> kerns;
+    cudaKernel_t tma_kern = nullptr;                // persistent bulk-copy variant of chunk 0 (if emitted)
+    std::map<int, int> tma_grid;                    // device -> resident CTAs (occupancy x SMs)
     std::set<int> attr_devices;          // devices on which smem attributes are set
     double compile_seconds = 0.0;
     int cache_hits = 0;
@@ -269,11 +271,13 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.team_smem = p->opts.team_smem;
     eo.groups = p->opts.groups;
     eo.cluster = p->opts.cluster;
+    eo.bulk_io = p->opts.bulk_io >= 0;
     eo.outline = p->opts.outline < 0 ? 0 : (p->opts.outline == 0 ? (eo.team >= 2 ? 3 : 0) : p->opts.outline);
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
     if (eo.outline) shape += "o" + std::to_string(eo.outline);
+    if (!eo.bulk_io) shape += "nb";
     v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
 
     std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
@@ -313,6 +317,8 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     return VSB_OK;
 }
 
+int sm_count(int device);
+
 int ensure_loaded(Variant* v, int device) {
     if (v->libs.empty()) {
         const size_t C = v->compiled.size();
@@ -328,6 +334,8 @@ int ensure_loaded(Variant* v, int device) {
             }
             CUDA_TRY(cudaLibraryGetKernel(&v->kerns[c], v->libs[c], v->ks.chunks[c].name.c_str()));
         }
+        if (C == 1 && v->ks.chunks[0].tma)
+            CUDA_TRY(cudaLibraryGetKernel(&v->tma_kern, v->libs[0], (v->ks.chunks[0].name + "_tma").c_str()));
     }
     if (!v->attr_devices.count(device)) {
         for (size_t c = 0; c < v->kerns.size(); ++c) {
@@ -335,6 +343,17 @@ int ensure_loaded(Variant* v, int device) {
             if (sm > 48 * 1024)
                 CUDA_TRY(cudaKernelSetAttributeForDevice(v->kerns[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          static_cast<int>(sm), device));
+        }
+        if (v->tma_kern) {
+            const int64_t sm = v->ks.chunks[0].tma_smem_bytes;
+            if (sm > 48 * 1024)
+                CUDA_TRY(cudaKernelSetAttributeForDevice(v->tma_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(sm), device));
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(v->tma_kern),
+                                                              v->ks.chunks[0].threads, static_cast<size_t>(sm)) != cudaSuccess)
+                per_sm = 0;
+            v->tma_grid[device] = per_sm * sm_count(device);
         }
         v->attr_devices.insert(device);
     }
@@ -409,6 +428,41 @@ int64_t chain_scratch_bytes(vsb_plan* p, Variant* v, int64_t n, int n_sm) {
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
                  int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device, void* scratch_pre = nullptr) {
     if (n <= 0) return VSB_OK;
+    // persistent TMA variant over the full 128-instance tiles (16-byte aligned I/O rows), the
+    // tail through the classic kernel below
+    static const bool no_tma = getenv("VSB_NO_TMA") != nullptr;
+    if (v->tma_kern && !no_tma && io_ld == 0) {
+        const auto& ch = v->ks.chunks[0];
+        const int64_t BSz = ch.threads, rs = p->rsz();
+        const int64_t nfull = n / BSz * BSz;
+        bool aligned = nfull > 0;
+        for (size_t i = 0; i < ins.size() && aligned; ++i)
+            if (p->prog.nnz_in[i]) aligned = ((reinterpret_cast<uintptr_t>(ins[i]) + e0 * p->prog.nnz_in[i] * rs) & 15) == 0;
+        for (size_t j = 0; j < outs.size() && aligned; ++j)
+            if (p->prog.nnz_out[j]) aligned = ((reinterpret_cast<uintptr_t>(outs[j]) + e0 * p->prog.nnz_out[j] * rs) & 15) == 0;
+        auto g = v->tma_grid.find(device);
+        if (aligned && g != v->tma_grid.end() && g->second > 0) {
+            const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+            std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
+            for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
+            for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
+            const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
+            pb[base + 1] = static_cast<uint64_t>(e0);
+            pb[base + 2] = static_cast<uint64_t>(nfull);
+            pb[base + 5] = static_cast<uint64_t>(BSz);
+            void* args[] = {pb.data()};
+            const int64_t grid = std::min<int64_t>(nfull / BSz, g->second);
+            cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->tma_kern), dim3(static_cast<unsigned>(grid)),
+                                             dim3(ch.threads), args, static_cast<size_t>(ch.tma_smem_bytes), stream);
+            if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + ch.name + "_tma): " + cudaGetErrorString(e));
+            if (nfull == n) return VSB_OK;
+            e0 += nfull;
+            n -= nfull;
+            std::vector<const void*> ins2(ins);
+            std::vector<void*> outs2(outs);
+            return launch_chain(p, v, ins2, outs2, e0, n, io_ld, stream, device, scratch_pre);
+        }
+    }
     int ipb_max = 32;
     for (auto& ch : v->ks.chunks) ipb_max = std::max(ipb_max, ch.inst_per_block);
     const int BS = ipb_max;
@@ -623,6 +677,10 @@ int64_t vsb_launches_per_eval(vsb_plan* p, int64_t n) {
     if (!p || n <= 0) return 0;
     std::lock_guard<std::mutex> lk(p->mu);
     Variant* v = p->variants.at(VSB_AOS).get();
+    if (v->tma_kern && !getenv("VSB_NO_TMA")) {
+        const int64_t bs = v->ks.chunks[0].threads;
+        return (n >= bs ? 1 : 0) + (n % bs ? 1 : 0);   // persistent TMA kernel + classic tail
+    }
     const int64_t wave = auto_wave(p, v, n);
     return static_cast<int64_t>(v->ks.chunks.size()) * ((n + wave - 1) / wave);
 }

@@ -43,7 +43,7 @@ class Plan:
 
     def __init__(self, tape, *, dtype="float64", block=0, chunk_ops=0, min_blocks=0, maxrregcount=0,
                  smem_budget=0, wave=0, compile_threads=0, verbose=False, cache_dir=None, team=0,
-                 phase_cost=0, priority=0, libdevice_trig=False, team_smem=0, groups=0, cluster=0, outline=0):
+                 phase_cost=0, priority=0, libdevice_trig=False, team_smem=0, groups=0, cluster=0, outline=0, bulk_io=0):
         self.tape: InstructionTape = as_tape(tape)
         self.dtype_code = _dtype_code(dtype)
         self.np_dtype = np.float32 if self.dtype_code == _native.VSB_F32 else np.float64
@@ -67,6 +67,7 @@ class Plan:
         opts.groups = int(groups)
         opts.cluster = int(cluster)
         opts.outline = int(outline)
+        opts.bulk_io = int(bulk_io)
         self._cache_dir = None if cache_dir is None else str(cache_dir).encode()
         opts.cache_dir = self._cache_dir
         code, values = self.tape.packed()
