@@ -300,3 +300,46 @@ def test_tma_tile_pipeline_equals_classic_kernel(name, B):
         ref = oracle.batch_eval(tape, ins)
         for a, r in zip(fast, ref):
             assert_close(a.cpu().numpy(), r, RTOL64, f"{name} B={B}")
+
+
+@pytest.mark.parametrize("name", ["cartpole_rk4", "ldlt_12", "srbm_mpc"])
+def test_batch_equals_serial_bitwise(name):
+    # test_batchrt.py:163-200: a batch row is bit-identical to serial_eval of that row
+    # (thread, TMA and team kernels alike)
+    tape = workloads.load_tape(name)
+    B = 4096 if name != "srbm_mpc" else 256
+    ins = workloads.make_inputs(name, B, seed=21)
+    batch = gpu_eval(tape, ins)
+    for row in (0, 1, B // 2, B - 1):
+        one = serial_eval(tape, [v[row] for v in ins])
+        for j, o in enumerate(one):
+            assert_bitwise_or_nan(batch[j][row], o, f"{name} row {row} out {j}")
+
+
+@pytest.mark.parametrize("name, team", [("cartpole_rk4", 0), ("humanoid_rbd", 0), ("srbm_mpc", 16)])
+def test_element_order_shuffling(name, team):
+    # test_batchrt.py:224-262: permuting the batch permutes the outputs, bit for bit
+    tape = workloads.load_tape(name)
+    B = 1000 if name != "srbm_mpc" else 300
+    ins = workloads.make_inputs(name, B, seed=22)
+    perm = np.random.default_rng(3).permutation(B)
+    opts = {"team": team} if team else {}
+    a = gpu_eval(tape, ins, **opts)
+    b = gpu_eval(tape, [v[perm] for v in ins], **opts)
+    for x, y in zip(a, b):
+        assert_bitwise_or_nan(x[perm], y, f"{name} permuted")
+
+
+def test_nan_and_inf_inputs_propagate_like_the_reference():
+    # test_batchrt.py:84-117 at tape level: non-finite inputs flow through sin/cos/div the
+    # same way (NaN == NaN, infinities exact)
+    tape = workloads.load_tape("cartpole_rk4")
+    ins = workloads.make_inputs("cartpole_rk4", 256, seed=23)
+    specials = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e308, -1e308, 5e-324]
+    for k, v in enumerate(specials):
+        ins[0][k * 4 % 256, k % 4] = v
+        ins[2][(k * 7 + 1) % 256, k % 4] = v
+    ref = oracle.batch_eval(tape, ins)
+    got = gpu_eval(tape, ins)
+    for g, r in zip(got, ref):
+        assert_close(g, r, RTOL64, "non-finite inputs")
