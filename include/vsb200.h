@@ -65,7 +65,8 @@ typedef struct vsb_options {
                                instruction cache instead of one per use): bit 0 DIV, bit 1
                                SIN/COS; 0 = auto (team mode: both), -1 = none              */
     int32_t bulk_io;        /* thread mode, single kernel: persistent TMA (cp.async.bulk) tile
-                               pipeline for the 128-instance tiles; 0 = auto (on), -1 = off */
+                               pipeline for the 128-instance tiles; 0 = auto (when every
+                               resident CTA gets >= 3 tiles), 1 = whenever aligned, -1 = off */
 } vsb_options;
 
 typedef struct vsb_plan vsb_plan;

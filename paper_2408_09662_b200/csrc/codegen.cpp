@@ -847,7 +847,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_tma(const VsArgs A) {\n", opt.min_blocks, nbuf);
                 b.put("    extern __shared__ __align__(128) real vs_smem[];\n");
                 b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", 2 * (IT + OT));
-                b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the runtime launches the tail separately\n");
+                b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the partial tail is done after the loop\n");
                 b.put("    if (threadIdx.x == 0) { vs_mbar_init(mbar, 1); vs_mbar_init(mbar + 1, 1); VS_FENCE_MBAR_INIT(); }\n");
                 b.put("    __syncthreads();\n");
                 // loads of one tile into buffer bs
@@ -918,6 +918,42 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 b.put("            VS_BULK_COMMIT();\n");
                 b.put("            if (tile + 2 * (long long)gridDim.x < ntiles) issue(tile + 2 * (long long)gridDim.x, bs);\n");
                 b.put("        }\n");
+                b.put("    }\n");
+                // the partial last tile (< 128 instances): one CTA, direct global loads/stores;
+                // spare threads mirror the last instance (benign duplicate stores)
+                b.put("    if (A.n %% VS_BS != 0 && blockIdx.x == (unsigned)(ntiles %% gridDim.x)) {\n");
+                b.put("        long long t = ntiles * VS_BS + threadIdx.x;\n");
+                b.put("        if (t >= A.n) t = A.n - 1;\n");
+                b.put("        const long long e = A.e0 + t;\n");
+                for (int i = 0; i < n_in; ++i)
+                    b.put("        const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n", i, i, p.nnz_in[i]);
+                for (int j = 0; j < n_out; ++j)
+                    b.put("        real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
+                for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
+                for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
+                {
+                    std::vector<uint8_t> done3(N, 0), got3(N, 0);
+                    auto ensure3 = [&](int32_t u) {
+                        const Node& nu = p.nodes[u];
+                        if (nu.op != OP_INPUT || got3[u]) return;
+                        got3[u] = 1;
+                        b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind2, u, nu.in_i, nu.in_k);
+                    };
+                    for (size_t si = 0; si < p.stores.size(); ++si) {
+                        const int32_t u = p.stores[si].node;
+                        if (p.nodes[u].op > OP_INPUT) continue;
+                        ensure3(u);
+                        b.put("%sO%d[%d] = %s;\n", ind2, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
+                    }
+                    for (int64_t q = ch.first; q < ch.last; ++q) {
+                        const Node& nd = p.nodes[q];
+                        if (nd.op <= OP_ASSIGN) continue;
+                        for (int k = 0; k < kArity[nd.op]; ++k) ensure3(nd.arg[k]);
+                        emit_def(b, q, done3, ind2);
+                        for (int32_t si : stores_of[q])
+                            b.put("%sO%d[%d] = v%" PRId64 ";\n", ind2, p.stores[si].j, p.stores[si].k, q);
+                    }
+                }
                 b.put("    }\n");
                 b.put("    if (threadIdx.x == 0) VS_BULK_WAIT_ALL();\n");
                 b.put("}\n");

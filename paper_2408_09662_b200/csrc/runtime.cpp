@@ -428,39 +428,36 @@ int64_t chain_scratch_bytes(vsb_plan* p, Variant* v, int64_t n, int n_sm) {
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
                  int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device, void* scratch_pre = nullptr) {
     if (n <= 0) return VSB_OK;
-    // persistent TMA variant over the full 128-instance tiles (16-byte aligned I/O rows), the
-    // tail through the classic kernel below
+    // persistent TMA variant: full 128-instance tiles through the bulk-copy pipeline, the
+    // partial tail inside the same launch.  Only when every resident CTA gets >= 3 tiles --
+    // below that the pipeline's prologue costs more than it hides (cartpole/pendulum
+    // B <= 3e5: classic faster; B = 1e6: TMA 1.05-1.19x; profiles/r1_sweeps_r32_tma_vs_batch.jsonl)
     static const bool no_tma = getenv("VSB_NO_TMA") != nullptr;
     if (v->tma_kern && !no_tma && io_ld == 0) {
         const auto& ch = v->ks.chunks[0];
         const int64_t BSz = ch.threads, rs = p->rsz();
-        const int64_t nfull = n / BSz * BSz;
-        bool aligned = nfull > 0;
-        for (size_t i = 0; i < ins.size() && aligned; ++i)
-            if (p->prog.nnz_in[i]) aligned = ((reinterpret_cast<uintptr_t>(ins[i]) + e0 * p->prog.nnz_in[i] * rs) & 15) == 0;
-        for (size_t j = 0; j < outs.size() && aligned; ++j)
-            if (p->prog.nnz_out[j]) aligned = ((reinterpret_cast<uintptr_t>(outs[j]) + e0 * p->prog.nnz_out[j] * rs) & 15) == 0;
         auto g = v->tma_grid.find(device);
-        if (aligned && g != v->tma_grid.end() && g->second > 0) {
+        const int64_t resident = g == v->tma_grid.end() ? 0 : g->second;
+        bool use = resident > 0 && (p->opts.bulk_io > 0 || n / BSz >= 3 * resident);  // bulk_io=1 forces it
+        for (size_t i = 0; i < ins.size() && use; ++i)
+            if (p->prog.nnz_in[i]) use = ((reinterpret_cast<uintptr_t>(ins[i]) + e0 * p->prog.nnz_in[i] * rs) & 15) == 0;
+        for (size_t j = 0; j < outs.size() && use; ++j)
+            if (p->prog.nnz_out[j]) use = ((reinterpret_cast<uintptr_t>(outs[j]) + e0 * p->prog.nnz_out[j] * rs) & 15) == 0;
+        if (use) {
             const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
             std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
             for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
             for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
             const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
             pb[base + 1] = static_cast<uint64_t>(e0);
-            pb[base + 2] = static_cast<uint64_t>(nfull);
+            pb[base + 2] = static_cast<uint64_t>(n);
             pb[base + 5] = static_cast<uint64_t>(BSz);
             void* args[] = {pb.data()};
-            const int64_t grid = std::min<int64_t>(nfull / BSz, g->second);
+            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(n / BSz, resident));
             cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->tma_kern), dim3(static_cast<unsigned>(grid)),
                                              dim3(ch.threads), args, static_cast<size_t>(ch.tma_smem_bytes), stream);
             if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + ch.name + "_tma): " + cudaGetErrorString(e));
-            if (nfull == n) return VSB_OK;
-            e0 += nfull;
-            n -= nfull;
-            std::vector<const void*> ins2(ins);
-            std::vector<void*> outs2(outs);
-            return launch_chain(p, v, ins2, outs2, e0, n, io_ld, stream, device, scratch_pre);
+            return VSB_OK;
         }
     }
     int ipb_max = 32;
@@ -678,8 +675,9 @@ int64_t vsb_launches_per_eval(vsb_plan* p, int64_t n) {
     std::lock_guard<std::mutex> lk(p->mu);
     Variant* v = p->variants.at(VSB_AOS).get();
     if (v->tma_kern && !getenv("VSB_NO_TMA")) {
-        const int64_t bs = v->ks.chunks[0].threads;
-        return (n >= bs ? 1 : 0) + (n % bs ? 1 : 0);   // persistent TMA kernel + classic tail
+        auto g = v->tma_grid.begin();
+        if (g != v->tma_grid.end() && (p->opts.bulk_io > 0 || n / v->ks.chunks[0].threads >= 3 * g->second))
+            return 1;  // one persistent launch
     }
     const int64_t wave = auto_wave(p, v, n);
     return static_cast<int64_t>(v->ks.chunks.size()) * ((n + wave - 1) / wave);

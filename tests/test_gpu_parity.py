@@ -291,9 +291,9 @@ def test_tma_tile_pipeline_equals_classic_kernel(name, B):
     tape = workloads.load_tape(name)
     ins = workloads.make_inputs(name, B, seed=B + 5)
     xs = [torch.tensor(v, device="cuda") for v in ins]
-    fast = vsb.Function(tape)(*xs)
+    fast = vsb.Function(tape, bulk_io=1)(*xs)       # force the TMA kernel at every size
     plain = vsb.Function(tape, bulk_io=-1)(*xs)
-    assert vsb.get_plan(tape).info["n_chunks"] == 1
+    assert vsb.get_plan(tape, bulk_io=1).info["n_chunks"] == 1
     for a, b in zip(fast, plain):
         assert_bitwise_or_nan(a.cpu().numpy(), b.cpu().numpy(), f"{name} B={B}")
     if B <= 4103:
@@ -343,3 +343,23 @@ def test_nan_and_inf_inputs_propagate_like_the_reference():
     got = gpu_eval(tape, ins)
     for g, r in zip(got, ref):
         assert_close(g, r, RTOL64, "non-finite inputs")
+
+
+@pytest.mark.parametrize("name", ["pendulum", "srbm_mpc"])
+def test_host_subranges_match_full(name):
+    # vsb_eval_host over [e0, e1) of a host workspace (what the INTEGRATION.md run_range stub
+    # issues per thread chunk) == the same rows of one full call, bit for bit
+    tape = workloads.load_tape(name)
+    B = 1000 if name == "pendulum" else 200
+    ins = workloads.make_inputs(name, B, seed=31)
+    full = gpu_eval(tape, ins)
+    ws = BatchWorkspace(tape, B)
+    for i, v in enumerate(ins):
+        ws.set_input(i, v)
+    for o in ws.outputs:
+        o[:] = np.nan
+    plan = Plan(tape)
+    for e0, e1 in [(0, 129), (129, 130), (130, 517), (517, B)] if B == 1000 else [(0, 37), (37, 64), (64, B)]:
+        plan.eval_host(ws._in_buf.ctypes.data, ws._in_off, ws._out_buf.ctypes.data, ws._out_off, e0, e1, 0)
+    for j in range(tape.n_out):
+        assert_bitwise_or_nan(ws.output_matrix(j), full[j], f"{name} out {j}")
