@@ -1204,6 +1204,38 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 }
                 allocate();
             }
+            if (getenv("VSB_LIVE_STATS")) {
+                // per-warp register live set: values defined by or loaded into warp w, live from
+                // definition/first load to their last use in w (stores count as uses)
+                int64_t worst = 0, sum_peak = 0;
+                for (int w = 0; w < W; ++w) {
+                    std::vector<int64_t> first(N, -1), lastu(N, -1);
+                    int64_t pos = 0;
+                    for (int ph = 0; ph < P; ++ph)
+                        for (int32_t q : ts.seq[w][ph]) {
+                            const Node& nd = p.nodes[q];
+                            for (int k = 0; k < kArity[nd.op]; ++k) {
+                                const int32_t u = nd.arg[k];
+                                if (p.nodes[u].op == OP_CONST) continue;
+                                if (first[u] < 0) first[u] = pos;
+                                lastu[u] = pos;
+                            }
+                            first[q] = pos;
+                            if (lastu[q] < pos) lastu[q] = pos;
+                            if (xend[q] >= 0 || slot_of[q] >= 0 || !stores_of[q].empty()) lastu[q] = std::max(lastu[q], pos + 1);
+                            ++pos;
+                        }
+                    std::vector<int64_t> delta(pos + 2, 0);
+                    for (int64_t q = 0; q < N; ++q)
+                        if (first[q] >= 0) { delta[first[q]] += 1; delta[lastu[q] + 1] -= 1; }
+                    int64_t run = 0, peak = 0;
+                    for (int64_t i = 0; i <= pos; ++i) { run += delta[i]; peak = std::max(peak, run); }
+                    worst = std::max(worst, peak);
+                    sum_peak += peak;
+                }
+                fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
+                        double(sum_peak) / W);
+            }
             ch.smem_slots = n_smem;
             ch.overflow_slots = n_glob;
             max_overflow = std::max(max_overflow, n_glob);
