@@ -557,7 +557,12 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     // auto: one thread per instance for small tapes; 12-warp teams above ~4k ops
     // (srbm_mpc B=4096: team 8 / 12 / 16 = 0.504 / 0.471 / 0.485 ms, profiles/r1_sweeps.jsonl)
     // (srbm_mpc 111k ops, B=4096, outlined DIV, profiles/r1_sweeps_r12.jsonl: team 16 / 12 = 0.402 / 0.418 ms)
-    if (p->opts.team == 0) p->opts.team = p->prog.n_live_ops >= 40000 ? 16 : p->prog.n_live_ops >= 4000 ? 12 : 1;
+    // wide tapes whose live set overflows the register file at 16 warps (duplicated cross-warp
+    // copies) run faster with 8 warps of 255 registers: rbd_chain12 (n_w 5816) team 8 / 16 / 32 =
+    // 0.72 / 1.15 / 1.80 ms (profiles/r1_sweeps_r34_config5.jsonl); n_w, the reference's work
+    // vector size, is its program-order live-set peak
+    if (p->opts.team == 0)
+        p->opts.team = p->prog.n_live_ops >= 40000 ? (p->prog.n_w > 4500 ? 8 : 16) : p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
     // thread mode, small tapes: 8 CTAs of 128 per SM (64 registers) hide the latency of the
     // per-thread dependency chains (cartpole_rk4 B=1e6: 0.096 -> 0.076 ms, pendulum 0.041 ->
