@@ -1204,7 +1204,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                 }
                 allocate();
             }
-            if (getenv("VSB_LIVE_STATS")) {
+            {
                 // per-warp register live set: values defined by or loaded into warp w, live from
                 // definition/first load to their last use in w (stores count as uses)
                 int64_t worst = 0, sum_peak = 0;
@@ -1233,8 +1233,10 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
                     worst = std::max(worst, peak);
                     sum_peak += peak;
                 }
-                fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
-                        double(sum_peak) / W);
+                if (getenv("VSB_LIVE_STATS"))
+                    fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
+                            double(sum_peak) / W);
+                ks.live_total = std::max(ks.live_total, sum_peak);  // ~ doubles per instance held in registers
             }
             ch.smem_slots = n_smem;
             ch.overflow_slots = n_glob;

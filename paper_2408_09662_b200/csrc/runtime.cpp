@@ -557,12 +557,8 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     // auto: one thread per instance for small tapes; 12-warp teams above ~4k ops
     // (srbm_mpc B=4096: team 8 / 12 / 16 = 0.504 / 0.471 / 0.485 ms, profiles/r1_sweeps.jsonl)
     // (srbm_mpc 111k ops, B=4096, outlined DIV, profiles/r1_sweeps_r12.jsonl: team 16 / 12 = 0.402 / 0.418 ms)
-    // wide tapes whose live set overflows the register file at 16 warps (duplicated cross-warp
-    // copies) run faster with 8 warps of 255 registers: rbd_chain12 (n_w 5816) team 8 / 16 / 32 =
-    // 0.72 / 1.15 / 1.80 ms (profiles/r1_sweeps_r34_config5.jsonl); n_w, the reference's work
-    // vector size, is its program-order live-set peak
-    if (p->opts.team == 0)
-        p->opts.team = p->prog.n_live_ops >= 40000 ? (p->prog.n_w > 4500 ? 8 : 16) : p->prog.n_live_ops >= 4000 ? 12 : 1;
+    const bool team_auto = p->opts.team == 0;
+    if (team_auto) p->opts.team = p->prog.n_live_ops >= 40000 ? 16 : p->prog.n_live_ops >= 4000 ? 12 : 1;
     if (p->opts.team == 1) p->opts.team = 0;
     // thread mode, small tapes: 8 CTAs of 128 per SM (64 registers) hide the latency of the
     // per-thread dependency chains (cartpole_rk4 B=1e6: 0.096 -> 0.076 ms, pendulum 0.041 ->
@@ -578,6 +574,19 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     if ((p->opts.team / p->opts.cluster) * p->opts.groups > 32)
         return fail(VSB_ERR_INVALID, "team / cluster * groups warps exceed 1024 threads per CTA");
     Variant* v = nullptr;
+    if (team_auto && p->opts.team == 16) {
+        // wide tapes whose registers-held live set at 16 warps (cross-warp copies duplicated in
+        // every consumer) is far past the register file run faster with 8 warps of 255
+        // registers: rbd_chain12 team 8 / 16 / 32 = 0.72 / 1.15 / 1.80 ms, live sum 2280 / 2704 /
+        // -; srbm_mpc stays at 16 (live sum 800; profiles/r1_sweeps_r34_config5.jsonl)
+        vsb::EmitOptions dry;
+        dry.team = 16;
+        dry.f32 = p->opts.dtype == VSB_F32;
+        dry.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
+        dry.team_smem = p->opts.team_smem;
+        dry.phase_cost = p->opts.phase_cost;
+        if (vsb::emit(p->prog, dry, "dry").live_total > 1500) p->opts.team = 8;
+    }
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
     *plan = p.release();
