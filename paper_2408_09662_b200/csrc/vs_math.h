@@ -414,7 +414,7 @@ VSM_FN int vsm_round_ok(vsm_dd y, double *out) {
 VSM_FN int vsm_fast_sc(vsm_dd r, double *s, double *c, int want) {
     double fi = VSM_RINT(r.hi * 64.0);
     int i = (int)fi + 52;
-    double th = r.hi - fi * 0.015625;              /* exact: fi/64 has <= 7 bits, same binade grid */
+    double th = VSM_FMA(-fi, 0.015625, r.hi);     /* exact: fi/64 has <= 7 bits, same binade grid */
     double tl = r.lo;
     double sah, sal, cah, cal;
     VSM_TAB(i, sah, sal, cah, cal);
@@ -426,14 +426,14 @@ VSM_FN int vsm_fast_sc(vsm_dd r, double *s, double *c, int want) {
     if (want & 1) {
         double ph = cah * th;
         double pl = VSM_FMA(cah, th, -ph);         /* CA_hi*th = ph + pl exactly */
-        vsm_dd h = vsm_two_sum(sah, ph);
+        vsm_dd h = vsm_fast_two_sum(sah, ph);     /* |SA| >= sin(1/64) > |CA*th| (or SA = 0) */
         double lo = h.lo + (pl + (sal + (sah * cm1 + (cah * tt + cal * th))));
         ok &= vsm_round_ok(vsm_fast_two_sum(h.hi, lo), s);
     }
     if (want & 2) {
         double qh = -sah * th;
         double ql = VSM_FMA(-sah, th, -qh);
-        vsm_dd g = vsm_two_sum(cah, qh);
+        vsm_dd g = vsm_fast_two_sum(cah, qh);     /* CA >= cos(0.8) > |SA*th| */
         double lo = g.lo + (ql + (cal + (cah * cm1 - (sah * tt + sal * th))));
         ok &= vsm_round_ok(vsm_fast_two_sum(g.hi, lo), c);
     }

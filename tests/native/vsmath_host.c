@@ -28,17 +28,17 @@ long h_fast_stats(const double *x, long n, double *max_rel_s, double *max_rel_c)
         /* recompute the unrounded fast values */
         double fi = VSM_RINT(r.hi * 64.0);
         int j = (int)fi + 52;
-        double th = r.hi - fi * 0.015625, tl = r.lo, sah, sal, cah, cal;
+        double th = VSM_FMA(-fi, 0.015625, r.hi), tl = r.lo, sah, sal, cah, cal;
         VSM_TAB(j, sah, sal, cah, cal);
         double t2 = th * th;
         double st = th * t2 * (VSM_F_S1 + t2 * (VSM_F_S2 + t2 * VSM_F_S3));
         double cm1 = VSM_FMA(-th, tl, t2 * (-0.5 + t2 * (VSM_F_C2 + t2 * VSM_F_C3)));
         double tt = tl + st;
         double ph = cah * th, pl = VSM_FMA(cah, th, -ph);
-        vsm_dd h = vsm_two_sum(sah, ph);
+        vsm_dd h = vsm_fast_two_sum(sah, ph);
         vsm_dd ys = vsm_fast_two_sum(h.hi, h.lo + (pl + (sal + (sah * cm1 + (cah * tt + cal * th)))));
         double qh = -sah * th, ql = VSM_FMA(-sah, th, -qh);
-        vsm_dd g = vsm_two_sum(cah, qh);
+        vsm_dd g = vsm_fast_two_sum(cah, qh);
         vsm_dd yc = vsm_fast_two_sum(g.hi, g.lo + (ql + (cal + (cah * cm1 - (sah * tt + sal * th)))));
         vsm_dd es = vsm_sin_kernel(r), ec = vsm_cos_kernel(r);
         vsm_dd ds = vsm_dd_add(ys, (vsm_dd){-es.hi, -es.lo});
