@@ -404,11 +404,17 @@ int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
     // ~1.05e11 distinct instr/s whether 128 or 148 SMs fetch), so spreading the same
     // instances over more CTAs only adds fetches (srbm_mpc B=4096 t16: 0.44 vs 0.40 ms)
     static const bool fill = getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) != 0;
+    // tiny batches (< 16 full CTAs): spread the instances over ~24 CTAs of >= 4 so that the
+    // SMs of a GPC fetch the same code and share the L1.5 instruction-cache fills
+    // (srbm_mpc B=100: 0.380 -> 0.324 ms; B >= 500 gains nothing; profiles/r1_sweeps_r45_spread.jsonl)
+    if (!fill && ks.cluster_dims_one() && (m + ipb - 1) / ipb < 16 && ipb >= 8)
+        return std::min<int64_t>(ipb, std::max<int64_t>(4, (m + 23) / 24));
     if (!fill) return ipb;
     const int64_t slots = std::max<int64_t>(1, n_sm / ch.cluster);  // co-resident clusters (1 CTA/SM)
     const int64_t waves = (((m + ipb - 1) / ipb) + slots - 1) / slots;
     int64_t ipc = (m + waves * slots - 1) / (waves * slots);
-    ipc = std::max<int64_t>(ipc, (ipb + 1) / 2);
+    static const int64_t ipc_min = getenv("VSB_IPC_MIN") ? atoll(getenv("VSB_IPC_MIN")) : 0;
+    ipc = std::max<int64_t>(ipc, ipc_min > 0 ? ipc_min : (ipb + 1) / 2);
     return std::min(ipb, ipc);
 }
 
