@@ -419,13 +419,25 @@ int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
 }
 
 // launch the kernel chain for elements [e0, e0+n) (indices relative to in/out pointers)
+// clusters (CTAs) launched for m instances: ceil(m / ipc), but at least 24 for tiny team
+// batches -- the extra CTAs recompute the last instance (benign duplicate stores) so that
+// ~24 SMs fetch the same code and share the L1.5 fills (srbm_mpc B=1 is the serial_eval path)
+int64_t units_for(const vsb::Kernelset& ks, int64_t m, int n_sm) {
+    if (m <= 0) return 0;
+    const int64_t c = pick_ipc(ks, m, n_sm);
+    const int64_t u = (m + c - 1) / c;
+    static const bool fill = getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) != 0;
+    if (ks.team >= 2 && !fill && ks.cluster_dims_one() && u < 24) return 24;
+    return u;
+}
+
 // bytes of SoA scratch a launch_chain over n instances needs (0 if none)
 int64_t chain_scratch_bytes(vsb_plan* p, Variant* v, int64_t n, int n_sm) {
     if (n <= 0 || v->ks.scratch_slots == 0) return 0;
     int ipb_max = 32;
     for (auto& ch : v->ks.chunks) ipb_max = std::max(ipb_max, ch.inst_per_block);
     const int64_t wave = auto_wave(p, v, n);
-    auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
+    auto units_of = [&](int64_t m) { return units_for(v->ks, m, n_sm); };
     const int64_t units = std::max(units_of(wave), units_of(n % wave));
     const int64_t ld_max = std::max<int64_t>((wave + ipb_max - 1) / ipb_max, units) * ipb_max;
     return ld_max * v->ks.scratch_slots * p->rsz();
@@ -474,7 +486,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     const int n_sm = sm_count(device);
     // every chunk of a variant has the same shape; scratch holds VS_IPB rows per cluster
     // (or block) of the biggest launch: a full wave or the remainder wave
-    auto units_of = [&](int64_t m) { const int64_t c = pick_ipc(v->ks, m, n_sm); return m > 0 ? (m + c - 1) / c : 0; };
+    auto units_of = [&](int64_t m) { return units_for(v->ks, m, n_sm); };
     void* scratch = scratch_pre;
     const int64_t units = std::max(units_of(wave), units_of(n % wave));
     const int64_t ld_max = std::max<int64_t>((wave + BS - 1) / BS, units) * BS;
@@ -500,7 +512,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
         void* args[] = {pb.data()};
         for (size_t c = 0; c < v->kerns.size(); ++c) {
             const auto& ch = v->ks.chunks[c];
-            const int64_t grid = (m + ipc - 1) / ipc * ch.cluster;
+            const int64_t grid = units_for(v->ks, m, n_sm) * ch.cluster;
             cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
                                              dim3(ch.threads), args, static_cast<size_t>(ch.smem_bytes), stream);
             if (e != cudaSuccess) {
