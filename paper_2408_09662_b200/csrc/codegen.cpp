@@ -452,25 +452,85 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
     return ts;
 }
 
-}  // namespace
+// One emit() call: whole-program analysis shared by all chunks (cuts, cross-chunk
+// scratch slots, SIN/COS pairs, I/O staging, the common source header), then each
+// chunk's kernel: thread mode (plus the persistent TMA variant) or team mode.
+class Emitter {
+public:
+    Emitter(const Program& prog, const EmitOptions& options, const std::string& kernel_tag)
+        : p(prog), opt(options), tag(kernel_tag) {}
+    Kernelset run();
 
-Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) {
+private:
+    // one team-mode chunk: schedule, barrier plan, cross-warp values and their rows
+    struct TeamPlan {
+        int W = 0, K = 1, G = 1, Wl = 0, IPB = 32, P = 0;
+        TeamSchedule ts;
+        std::vector<int32_t> warp_of, phase_of;
+        bool split = false;
+        std::vector<int32_t> sync_at;
+        std::vector<std::vector<int8_t>> end_act;
+        std::vector<std::vector<int32_t>> syncb;
+        std::vector<std::vector<int32_t>> extra_stores;
+        std::vector<int32_t> xend;
+        std::vector<uint32_t> xranks;
+        std::vector<std::vector<int32_t>> xcons;
+        std::vector<int32_t> xvals;
+        std::vector<uint8_t> to_global;
+        std::vector<int32_t> mate;
+        std::vector<uint8_t> second;
+        std::vector<int32_t> xslot;
+        int64_t cap = 0, n_smem = 0, n_glob = 0;
+        bool pairing = false;
+        bool in_chunk(const Program& p, const Chunk& ch, int32_t u) const {
+            return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN;
+        }
+    };
+
+    const Program& p;
+    const EmitOptions& opt;
+    const std::string& tag;
     Kernelset ks;
-    ks.block = opt.block;
-    ks.f32 = opt.f32;
-    ks.layout = opt.layout;
-    const bool team = opt.team >= 2;
-    ks.team = team ? opt.team : 0;
-    const int64_t N = static_cast<int64_t>(p.nodes.size());
-    const int n_in = static_cast<int>(p.nnz_in.size());
-    const int n_out = static_cast<int>(p.nnz_out.size());
-    const bool f32 = opt.f32;
-    const int rsz = f32 ? 4 : 8;
-    const char* real = f32 ? "float" : "double";
-    const bool soa = opt.layout == Layout::SOA;
+    bool team = false, f32 = false, soa = false, trig_exact = false, out_div = false, out_trig = false;
+    int64_t N = 0;
+    int n_in = 0, n_out = 0, rsz = 8;
+    const char* real = "double";
+    const char* fs = "";
+    std::vector<int64_t> opcum, cuts;
+    int C = 0;
+    std::vector<int32_t> def_chunk, last_chunk, slot_of, partner, loaded_in;
+    std::vector<std::vector<int32_t>> stores_of;
+    std::vector<uint8_t> done;
+    int64_t cross_slots = 0, max_overflow = 0;
+    int64_t ni_tot = 0, no_tot = 0, SI = 1, SO = 1, in_bytes = 0, out_bytes = 0;
+    bool stage_in = false, stage_out = false, same_kernel = false;
+    int TK = 1, TG = 1, TWl = 0;
+    Out hdr;
 
-    // ---- chunk boundaries over node positions --------------------------------
-    std::vector<int64_t> opcum(N + 1, 0);
+    void cut_chunks();
+    void plan_cross_chunk();
+    void plan_staging();
+    void build_header();
+    std::string opnd(int32_t u) const;
+    std::string expr_of(const Node& nd) const;
+    void emit_def(Out& b, int64_t q, std::vector<uint8_t>& done, const char* ind) const;
+    void emit_store(Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) const;
+    void input_load(Out& o, int32_t u, const char* ind) const;
+    void io_bases(Out& o) const;
+    void emit_direct_body(Out& b, const Chunk& ch, bool ldg) const;
+    void emit_thread_chunk(int c, Chunk& ch, Out& b);
+    void emit_tma_kernel(Chunk& ch, Out& b) const;
+    void emit_team_chunk(int c, Chunk& ch, Out& b);
+    void team_barrier_plan(TeamPlan& tp, const Chunk& ch);
+    void team_cross_warp_values(TeamPlan& tp, Chunk& ch, int c);
+    void team_rows(TeamPlan& tp, Chunk& ch);
+    void team_live_stats(TeamPlan& tp, int c);
+    void team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b);
+};
+
+// ---- chunk boundaries over node positions ----------------------------------------
+void Emitter::cut_chunks() {
+    opcum.assign(N + 1, 0);
     for (int64_t q = 0; q < N; ++q) opcum[q + 1] = opcum[q] + (p.nodes[q].op > OP_ASSIGN ? 1 : 0);
     const int64_t total_ops = opcum[N];
     int64_t K = opt.chunk_ops;
@@ -497,7 +557,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         int64_t run = 0;
         for (int64_t c = 0; c <= N; ++c) { run += delta[c]; across[c] = run; }
     }
-    std::vector<int64_t> cuts = {0};
+    cuts = {0};
     if (total_ops > K) {
         int64_t pos = 0;
         while (opcum[N] - opcum[pos] > K + K / 4) {
@@ -514,12 +574,15 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         }
     }
     cuts.push_back(N);
-    const int C = static_cast<int>(cuts.size()) - 1;
+    C = static_cast<int>(cuts.size()) - 1;
+}
 
-    // ---- cross-chunk values and their SoA scratch slots ----------------------
-    // thread mode stages inputs in chunk 0 and exports the ones later chunks
-    // need; team mode re-loads inputs from global in every chunk
-    std::vector<int32_t> def_chunk(N, -1), last_chunk(N, -1);
+// ---- cross-chunk values and their SoA scratch slots; stores; SIN/COS pairs --------
+// thread mode stages inputs in chunk 0 and exports the ones later chunks
+// need; team mode re-loads inputs from global in every chunk
+void Emitter::plan_cross_chunk() {
+    def_chunk.assign(N, -1);
+    last_chunk.assign(N, -1);
     for (int c = 0; c < C; ++c)
         for (int64_t q = cuts[c]; q < cuts[c + 1]; ++q) def_chunk[q] = c;
     for (int64_t q = 0; q < N; ++q)
@@ -535,7 +598,7 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         }
     for (const Store& s : p.stores)
         if (p.nodes[s.node].op != OP_CONST) last_chunk[s.node] = std::max(last_chunk[s.node], C - 1);
-    std::vector<int32_t> slot_of(N, -1);
+    slot_of.assign(N, -1);
     {
         std::vector<std::vector<int32_t>> born(C), dies(C);
         for (int64_t q = 0; q < N; ++q)
@@ -555,14 +618,14 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         }
         ks.scratch_slots = next;
     }
-    const int64_t cross_slots = ks.scratch_slots;
+    cross_slots = ks.scratch_slots;
 
     // stores grouped per defining node ("store at definition")
-    std::vector<std::vector<int32_t>> stores_of(N);
+    stores_of.assign(N, {});
     for (size_t s = 0; s < p.stores.size(); ++s) stores_of[p.stores[s].node].push_back(static_cast<int32_t>(s));
 
     // SIN/COS of the same value share one argument reduction (vs_sincos)
-    std::vector<int32_t> partner(N, -1);
+    partner.assign(N, -1);
     {
         std::unordered_map<int32_t, int32_t> sin_of, cos_of;
         for (int64_t q = 0; q < N; ++q) {
@@ -579,15 +642,19 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
             partner[b] = a;
         }
     }
-    const bool trig_exact = opt.exact_trig && !f32;
+}
 
-    // ---- I/O staging decisions (thread mode) ----------------------------------
-    const int64_t ni_tot = p.in_base[n_in], no_tot = p.out_base[n_out];
-    const int64_t SI = ni_tot | 1, SO = no_tot | 1;
-    int64_t in_bytes = team || soa || ni_tot == 0 ? 0 : SI * opt.block * rsz;
-    int64_t out_bytes = team || soa || no_tot == 0 ? 0 : SO * opt.block * rsz;
-    bool stage_in = in_bytes > 0, stage_out = out_bytes > 0;
-    const bool same_kernel = (C == 1);
+// ---- I/O staging decisions (thread mode) --------------------------------------------
+void Emitter::plan_staging() {
+    ni_tot = p.in_base[n_in];
+    no_tot = p.out_base[n_out];
+    SI = ni_tot | 1;
+    SO = no_tot | 1;
+    in_bytes = team || soa || ni_tot == 0 ? 0 : SI * opt.block * rsz;
+    out_bytes = team || soa || no_tot == 0 ? 0 : SO * opt.block * rsz;
+    stage_in = in_bytes > 0;
+    stage_out = out_bytes > 0;
+    same_kernel = (C == 1);
     auto fits = [&]() {
         const int64_t a = stage_in ? in_bytes : 0, b = stage_out ? out_bytes : 0;
         return (same_kernel ? a + b : std::max(a, b)) <= opt.smem_budget;
@@ -599,12 +666,13 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         if (stage_in && in_bytes > opt.smem_budget) stage_in = false;
         if (stage_out && out_bytes > opt.smem_budget) stage_out = false;
     }
+}
 
-    // ---- common source header ---------------------------------------------------
-    Out hdr;
-    const int TK = team ? std::max(1, opt.cluster) : 1;     // CTAs per cluster
-    const int TG = team ? std::max(1, opt.groups) : 1;      // instance groups per CTA
-    const int TWl = team ? opt.team / TK : 0;               // warp streams per CTA
+// ---- common source header ------------------------------------------------------------
+void Emitter::build_header() {
+    TK = team ? std::max(1, opt.cluster) : 1;     // CTAs per cluster
+    TG = team ? std::max(1, opt.groups) : 1;      // instance groups per CTA
+    TWl = team ? opt.team / TK : 0;               // warp streams per CTA
     ks.groups = TG;
     ks.cluster = TK;
     hdr.put("#define VS_BS %d\n", team ? TWl * TG * 32 : opt.block);
@@ -628,8 +696,8 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
         hdr.s += kVsMathSource;
         hdr.s += "\n";
     }
-    const bool out_div = (opt.outline & 1) != 0;
-    const bool out_trig = (opt.outline & 2) != 0 && trig_exact;
+    out_div = (opt.outline & 1) != 0;
+    out_trig = (opt.outline & 2) != 0 && trig_exact;
     if (out_div) hdr.s += "__device__ __noinline__ real vs_div_o(real a, real b) { return a / b; }\n";
     if (out_trig)
         hdr.s += "__device__ __noinline__ double vs_sin_o(double x) { return vs_sin(x); }\n"
@@ -639,727 +707,836 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
             "    long long e0, n, ld, io_ld, ipc;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
     ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc";
+}
 
-    const char* fs = f32 ? "f" : "";
-    auto opnd = [&](int32_t u) -> std::string {
-        const Node& nu = p.nodes[u];
-        if (nu.op == OP_CONST) return literal(nu.imm, f32);
-        return "v" + std::to_string(u);
-    };
-    // expression of one op (SIN/COS handled separately for pairing)
-    auto expr_of = [&](const Node& nd) -> std::string {
-        const int ar = kArity[nd.op];
-        const std::string x = ar > 0 ? opnd(nd.arg[0]) : "", y = ar > 1 ? opnd(nd.arg[1]) : "",
-                          z = ar > 2 ? opnd(nd.arg[2]) : "";
-        const char* X = x.c_str(); const char* Y = y.c_str(); const char* Z = z.c_str();
-        char eb[1024];
-        switch (nd.op) {
-        case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
-        case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
-        case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
-        case OP_DIV: snprintf(eb, sizeof eb, out_div ? "vs_div_o(%s, %s)" : "%s / %s", X, Y); break;
-        case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
-        case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
-        case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
-        case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
-        case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
-        case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
-        case OP_SIN:
-            if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_sin_o(%s)" : "vs_sin(%s)", X);
-            else snprintf(eb, sizeof eb, "sin%s(%s)", fs, X);
-            break;
-        case OP_COS:
-            if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_cos_o(%s)" : "vs_cos(%s)", X);
-            else snprintf(eb, sizeof eb, "cos%s(%s)", fs, X);
-            break;
-        case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
-        case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
-        case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
-        case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
-        case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;
-        case OP_STEP: snprintf(eb, sizeof eb, "(%s > (real)0) ? (real)1 : (real)0", X); break;
-        case OP_IF_ELSE: snprintf(eb, sizeof eb, "(%s != (real)0) ? %s : %s", X, Y, Z); break;
-        default: snprintf(eb, sizeof eb, "%s", X); break;
-        }
-        return eb;
-    };
-    // emit the definition of node q (pairs SIN/COS); `done` marks nodes already defined
-    auto emit_def = [&](Out& b, int64_t q, std::vector<uint8_t>& done, const char* ind) {
-        if (done[q]) return;
-        const Node& nd = p.nodes[q];
-        const int32_t mate = partner[q];
-        if (mate >= 0 && !done[mate]) {
-            const int32_t sn = nd.op == OP_SIN ? static_cast<int32_t>(q) : mate;
-            const int32_t cn = nd.op == OP_SIN ? mate : static_cast<int32_t>(q);
-            const std::string x = opnd(nd.arg[0]);
-            if (out_trig) {
-                b.put("%sconst vs_sc sc%d = vs_sincos_o(%s);\n", ind, sn, x.c_str());
-                b.put("%sconst real v%d = sc%d.s, v%d = sc%d.c;\n", ind, sn, sn, cn, sn);
-                done[sn] = done[cn] = 1;
-                return;
-            }
-            b.put("%sreal v%d, v%d;\n", ind, sn, cn);
-            b.put("%s%s(%s, &v%d, &v%d);\n", ind, trig_exact ? "vs_sincos" : (f32 ? "sincosf" : "sincos"), x.c_str(), sn, cn);
+std::string Emitter::opnd(int32_t u) const {
+    const Node& nu = p.nodes[u];
+    if (nu.op == OP_CONST) return literal(nu.imm, f32);
+    return "v" + std::to_string(u);
+}
+
+// expression of one op (SIN/COS handled separately for pairing)
+std::string Emitter::expr_of(const Node& nd) const {
+    const int ar = kArity[nd.op];
+    const std::string x = ar > 0 ? opnd(nd.arg[0]) : "", y = ar > 1 ? opnd(nd.arg[1]) : "",
+                      z = ar > 2 ? opnd(nd.arg[2]) : "";
+    const char* X = x.c_str(); const char* Y = y.c_str(); const char* Z = z.c_str();
+    char eb[1024];
+    switch (nd.op) {
+    case OP_ADD: snprintf(eb, sizeof eb, "%s + %s", X, Y); break;
+    case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
+    case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
+    case OP_DIV: snprintf(eb, sizeof eb, out_div ? "vs_div_o(%s, %s)" : "%s / %s", X, Y); break;
+    case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
+    case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
+    case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
+    case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
+    case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
+    case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
+    case OP_SIN:
+        if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_sin_o(%s)" : "vs_sin(%s)", X);
+        else snprintf(eb, sizeof eb, "sin%s(%s)", fs, X);
+        break;
+    case OP_COS:
+        if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_cos_o(%s)" : "vs_cos(%s)", X);
+        else snprintf(eb, sizeof eb, "cos%s(%s)", fs, X);
+        break;
+    case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
+    case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
+    case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
+    case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
+    case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;
+    case OP_STEP: snprintf(eb, sizeof eb, "(%s > (real)0) ? (real)1 : (real)0", X); break;
+    case OP_IF_ELSE: snprintf(eb, sizeof eb, "(%s != (real)0) ? %s : %s", X, Y, Z); break;
+    default: snprintf(eb, sizeof eb, "%s", X); break;
+    }
+    return eb;
+}
+
+// emit the definition of node q (pairs SIN/COS); `done` marks nodes already defined
+void Emitter::emit_def(Out& b, int64_t q, std::vector<uint8_t>& done, const char* ind) const {
+    if (done[q]) return;
+    const Node& nd = p.nodes[q];
+    const int32_t mate = partner[q];
+    if (mate >= 0 && !done[mate]) {
+        const int32_t sn = nd.op == OP_SIN ? static_cast<int32_t>(q) : mate;
+        const int32_t cn = nd.op == OP_SIN ? mate : static_cast<int32_t>(q);
+        const std::string x = opnd(nd.arg[0]);
+        if (out_trig) {
+            b.put("%sconst vs_sc sc%d = vs_sincos_o(%s);\n", ind, sn, x.c_str());
+            b.put("%sconst real v%d = sc%d.s, v%d = sc%d.c;\n", ind, sn, sn, cn, sn);
             done[sn] = done[cn] = 1;
             return;
         }
-        b.put("%sconst real v%" PRId64 " = %s;\n", ind, q, expr_of(nd).c_str());
-        done[q] = 1;
+        b.put("%sreal v%d, v%d;\n", ind, sn, cn);
+        b.put("%s%s(%s, &v%d, &v%d);\n", ind, trig_exact ? "vs_sincos" : (f32 ? "sincosf" : "sincos"), x.c_str(), sn, cn);
+        done[sn] = done[cn] = 1;
+        return;
+    }
+    b.put("%sconst real v%" PRId64 " = %s;\n", ind, q, expr_of(nd).c_str());
+    done[q] = 1;
+}
+
+void Emitter::emit_store(Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) const {
+        const Store& s = p.stores[s_idx];
+        if (staged) {
+            o.put("%sorow[%" PRId64 "] = %s;\n", ind, p.out_base[s.j] + s.k, val.c_str());
+        } else if (soa) {
+            o.put("%sO%d[(long long)%d * A.io_ld] = %s;\n", ind, s.j, s.k, val.c_str());
+        } else {
+            o.put("%sO%d[%d] = %s;\n", ind, s.j, s.k, val.c_str());  // immediate offset
+        }
+}
+
+void Emitter::input_load(Out& o, int32_t u, const char* ind) const {
+        const Node& nu = p.nodes[u];
+        if (soa)
+            o.put("%sconst real v%d = __ldg(I%d + (long long)%d * A.io_ld);\n", ind, u, nu.in_i, nu.in_k);
+        else
+            o.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
+}
+
+// per-thread base pointers of every input/output row (hoisted address math)
+void Emitter::io_bases(Out& o) const {
+        for (int i = 0; i < n_in; ++i)
+            o.put(soa ? "    const real* __restrict__ I%d = A.in[%d] + e;\n"
+                      : "    const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n",
+                  i, i, p.nnz_in[i]);
+        for (int j = 0; j < n_out; ++j)
+            o.put(soa ? "    real* __restrict__ O%d = A.out[%d] + e;\n"
+                      : "    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n",
+                  j, j, p.nnz_out[j]);
+        for (int i = 0; i < n_in; ++i) o.put("    (void)I%d;\n", i);
+        for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
+}
+
+void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg) const {
+    // ops of the chunk with direct I/O: inputs `I<i>[k]` (smem tile row) or `__ldg(I<i> + k)`
+    // (global row), outputs `O<j>[k] = v`; one thread per instance, no scratch
+    const char* ind = "        ";
+    std::vector<uint8_t> dn(N, 0), got(N, 0);
+    auto ensure = [&](int32_t u) {
+        const Node& nu = p.nodes[u];
+        if (nu.op != OP_INPUT || got[u]) return;
+        got[u] = 1;
+        if (ldg) b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
+        else b.put("%sconst real v%d = I%d[%d];\n", ind, u, nu.in_i, nu.in_k);
     };
+    for (size_t si = 0; si < p.stores.size(); ++si) {
+        const int32_t u = p.stores[si].node;
+        if (p.nodes[u].op > OP_INPUT) continue;
+        ensure(u);
+        b.put("%sO%d[%d] = %s;\n", ind, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
+    }
+    for (int64_t q = ch.first; q < ch.last; ++q) {
+        const Node& nd = p.nodes[q];
+        if (nd.op <= OP_ASSIGN) continue;
+        for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+        emit_def(b, q, dn, ind);
+        for (int32_t si : stores_of[q])
+            b.put("%sO%d[%d] = v%" PRId64 ";\n", ind, p.stores[si].j, p.stores[si].k, q);
+    }
+}
 
-    std::vector<int32_t> loaded_in(N, -1);  // thread mode: chunk in which a value is available
-    std::vector<uint8_t> done(N, 0);
-    int64_t max_overflow = 0;
+// ================= one thread per instance =================
+void Emitter::emit_thread_chunk(int c, Chunk& ch, Out& b) {
+    const bool first = (c == 0), last = (c == C - 1);
+    ch.stage_in = first && stage_in;
+    ch.stage_out = last && stage_out;
+    ch.threads = opt.block;
+    ch.inst_per_block = opt.block;
+    const int64_t sin_off = 0;
+    const int64_t sout_off = ch.stage_in ? SI * opt.block : 0;
+    ch.smem_bytes = (ch.stage_in ? in_bytes : 0) + (ch.stage_out ? out_bytes : 0);
+    b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, ch.name.c_str());
+    b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
+    // spare threads of the last block mirror the last instance: same inputs, same
+    // bits, so their (duplicate) stores are benign and no load/store needs a guard
+    b.put("    long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
+    b.put("    if (t >= A.n) t = A.n - 1;\n");
+    b.put("    const long long e = A.e0 + t;\n");
+    b.put("    (void)e;\n");
+    io_bases(b);
+    // block-local SoA scratch [block][slot][VS_IPB]: slot offsets are immediates
+    if (ks.scratch_slots > 0)
+        b.put("    real* __restrict__ S = A.scratch + (long long)blockIdx.x * (VS_NSLOT * VS_IPB) + threadIdx.x;\n");
+    if (ch.stage_in || ch.stage_out) {
+        b.put("    const long long blk0 = (long long)blockIdx.x * VS_BS;\n");
+        b.put("    const int nblk = (int)((A.n - blk0) < VS_BS ? (A.n - blk0) : VS_BS);\n");
+    }
+    if (ch.stage_in) {
+        for (int i = 0; i < n_in; ++i) {
+            if (p.nnz_in[i] == 0) continue;
+            b.put("    vs_stage_in<%" PRId64 ", %" PRId64 ", %" PRId64 ">(vs_smem + %" PRId64 ", A.in[%d] + (A.e0 + blk0) * %" PRId64 "LL, nblk * %" PRId64 ");\n",
+                  p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
+        }
+        b.put("    __syncthreads();\n");
+        // spare threads of the last block read the last staged row (they mirror instance n-1,
+        // whose outputs they may store when outputs are not staged)
+        b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + (threadIdx.x < nblk ? threadIdx.x : nblk - 1) * %" PRId64 ";\n", sin_off, SI);
+    }
+    if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
 
+    std::function<void(int32_t)> ensure = [&](int32_t u) {
+        const Node& nu = p.nodes[u];
+        if (nu.op == OP_CONST || loaded_in[u] == c) return;
+        loaded_in[u] = c;
+        if (def_chunk[u] < c || (nu.op == OP_INPUT && !first)) {
+            b.put("    const real v%d = S[%d * VS_IPB];\n", u, slot_of[u]);
+            ++ch.loads;
+            return;
+        }
+        if (ch.stage_in) b.put("    const real v%d = srow[%" PRId64 "];\n", u, p.in_base[nu.in_i] + nu.in_k);
+        else input_load(b, u, "    ");
+        if (slot_of[u] >= 0 && first) { b.put("    S[%d * VS_IPB] = v%d;\n", slot_of[u], u); ++ch.stores; }
+    };
+    if (first)
+        for (int64_t q = 0; q < N; ++q)
+            if (p.nodes[q].op == OP_INPUT && slot_of[q] >= 0) ensure(static_cast<int32_t>(q));
+    if (last) {
+        for (size_t s = 0; s < p.stores.size(); ++s) {
+            const int32_t u = p.stores[s].node;
+            const Node& nu = p.nodes[u];
+            if (nu.op > OP_INPUT && def_chunk[u] == c) continue;
+            ensure(u);
+            emit_store(b, static_cast<int32_t>(s), opnd(u), "    ", ch.stage_out);
+        }
+    }
+    for (int64_t q = ch.first; q < ch.last; ++q) {
+        const Node& nd = p.nodes[q];
+        if (nd.op <= OP_ASSIGN) continue;
+        for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+        emit_def(b, q, done, "    ");
+        loaded_in[q] = c;
+        if (slot_of[q] >= 0) { b.put("    S[%d * VS_IPB] = v%" PRId64 ";\n", slot_of[q], q); ++ch.stores; }
+        if (last)
+            for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), "    ", ch.stage_out);
+    }
+    if (ch.stage_out) {
+        b.put("    __syncthreads();\n");
+        for (int j = 0; j < n_out; ++j) {
+            if (p.nnz_out[j] == 0) continue;
+            b.put("    vs_stage_out<%" PRId64 ", %" PRId64 ", %" PRId64 ">(A.out[%d] + (A.e0 + blk0) * %" PRId64 "LL, vs_smem + %" PRId64 ", nblk * %" PRId64 ");\n",
+                  p.nnz_out[j], p.out_base[j], SO, j, p.nnz_out[j], sout_off, p.nnz_out[j]);
+        }
+    }
+    b.put("}\n");
+    // ---- persistent TMA variant: full 128-instance tiles stream through two smem
+    // buffers with cp.async.bulk (one bulk copy per input / output array, completion on
+    // an mbarrier), the next tiles' loads in flight while the current tile computes
+    const bool tma = opt.bulk_io && same_kernel && !soa && ni_tot > 0 && no_tot > 0 &&
+                     2 * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
+    if (tma) emit_tma_kernel(ch, b);
+}
+
+void Emitter::emit_tma_kernel(Chunk& ch, Out& b) const {
+    ch.tma = true;
+    const int64_t IT = ni_tot * opt.block, OT = no_tot * opt.block;  // tile sizes (elements)
+    ch.tma_smem_bytes = 2 * (IT + OT) * rsz + 16;
+    b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_tma(const VsArgs A) {\n", opt.min_blocks, ch.name.c_str());
+    b.put("    extern __shared__ __align__(128) real vs_smem[];\n");
+    b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", 2 * (IT + OT));
+    b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the partial tail is done after the loop\n");
+    b.put("    if (threadIdx.x == 0) { vs_mbar_init(mbar, 1); vs_mbar_init(mbar + 1, 1); VS_FENCE_MBAR_INIT(); }\n");
+    b.put("    __syncthreads();\n");
+    // loads of one tile into buffer bs
+    Out ld;
+    ld.put("    auto issue = [&](long long tile, int bs) {\n");
+    ld.put("        real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
+    ld.put("        const long long e = A.e0 + tile * VS_BS;\n");
+    ld.put("        vs_mbar_expect(mbar + bs, %" PRId64 "u);\n", IT * rsz);
+    for (int i = 0; i < n_in; ++i) {
+        if (p.nnz_in[i] == 0) continue;
+        ld.put("        vs_bulk_load(ib + %" PRId64 ", A.in[%d] + e * %" PRId64 "LL, %" PRId64 "u, mbar + bs);\n",
+               p.in_base[i] * opt.block, i, p.nnz_in[i], p.nnz_in[i] * opt.block * rsz);
+    }
+    ld.put("    };\n");
+    b.s += ld.s;
+    b.put("    long long tile = blockIdx.x;\n");
+    b.put("    if (threadIdx.x == 0) {\n");
+    b.put("        if (tile < ntiles) issue(tile, 0);\n");
+    b.put("        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);\n");
+    b.put("    }\n");
+    b.put("    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {\n");
+    b.put("        const int bs = k & 1;\n");
+    b.put("        vs_mbar_wait(mbar + bs, (k >> 1) & 1);\n");
+    b.put("        if (threadIdx.x == 0 && k >= 2) VS_BULK_WAIT_READ1();  // out buffer bs free again\n");
+    b.put("        __syncthreads();\n");
+    b.put("        const real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
+    b.put("        real* ob = vs_smem + %" PRId64 " + bs * %" PRId64 ";\n", 2 * IT, OT);
+    for (int i = 0; i < n_in; ++i)
+        b.put("        const real* __restrict__ I%d = ib + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", i,
+              p.in_base[i] * opt.block, p.nnz_in[i]);
+    for (int j = 0; j < n_out; ++j)
+        b.put("        real* __restrict__ O%d = ob + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", j,
+              p.out_base[j] * opt.block, p.nnz_out[j]);
+    for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
+    for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
+    // body: same op sequence, inputs from the smem tile row, outputs to the smem out row
+    emit_direct_body(b, ch, false);
+    b.put("        VS_FENCE_ASYNC();   // generic-proxy smem writes -> visible to the bulk store\n");
+    b.put("        __syncthreads();\n");
+    b.put("        if (threadIdx.x == 0) {\n");
+    b.put("            const long long e = A.e0 + tile * VS_BS;\n");
+    for (int j = 0; j < n_out; ++j) {
+        if (p.nnz_out[j] == 0) continue;
+        b.put("            vs_bulk_store(A.out[%d] + e * %" PRId64 "LL, ob + %" PRId64 ", %" PRId64 "u);\n", j,
+              p.nnz_out[j], p.out_base[j] * opt.block, p.nnz_out[j] * opt.block * rsz);
+    }
+    b.put("            VS_BULK_COMMIT();\n");
+    b.put("            if (tile + 2 * (long long)gridDim.x < ntiles) issue(tile + 2 * (long long)gridDim.x, bs);\n");
+    b.put("        }\n");
+    b.put("    }\n");
+    // the partial last tile (< 128 instances): one CTA, direct global loads/stores;
+    // spare threads mirror the last instance (benign duplicate stores)
+    b.put("    if (A.n %% VS_BS != 0 && blockIdx.x == (unsigned)(ntiles %% gridDim.x)) {\n");
+    b.put("        long long t = ntiles * VS_BS + threadIdx.x;\n");
+    b.put("        if (t >= A.n) t = A.n - 1;\n");
+    b.put("        const long long e = A.e0 + t;\n");
+    for (int i = 0; i < n_in; ++i)
+        b.put("        const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n", i, i, p.nnz_in[i]);
+    for (int j = 0; j < n_out; ++j)
+        b.put("        real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
+    for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
+    for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
+    emit_direct_body(b, ch, true);
+    b.put("    }\n");
+    b.put("    if (threadIdx.x == 0) VS_BULK_WAIT_ALL();\n");
+    b.put("}\n");
+}
+
+// ================= team mode: W warps x 32 instances =================
+void Emitter::emit_team_chunk(int c, Chunk& ch, Out& b) {
+    TeamPlan tp;
+    tp.W = opt.team;
+    tp.K = TK;
+    tp.G = TG;
+    tp.Wl = TWl;
+    ch.threads = tp.Wl * tp.G * 32;
+    ch.inst_per_block = 32 * tp.G;
+    ch.cluster = tp.K;
+    tp.IPB = 32 * tp.G;
+    tp.warp_of.assign(N, -1);
+    tp.phase_of.assign(N, -1);
+    tp.ts = schedule_team(p, ch.first, ch.last, tp.W, std::max(1, opt.phase_cost), opt.priority,
+                          tp.K > 1 ? tp.Wl : 0, tp.warp_of, tp.phase_of);
+    tp.P = tp.ts.P;
+    ch.phases = tp.P;
+    team_barrier_plan(tp, ch);
+    team_cross_warp_values(tp, ch, c);
+    team_rows(tp, ch);
+    team_live_stats(tp, c);
+    team_kernel_source(tp, c, ch, b);
+}
+
+void Emitter::team_barrier_plan(TeamPlan& tp, const Chunk& ch) {
+    auto& W = tp.W;
+    auto& K = tp.K;
+    auto& P = tp.P;
+    auto& ts = tp.ts;
+    auto& warp_of = tp.warp_of;
+    auto& phase_of = tp.phase_of;
+    auto& sync_at = tp.sync_at;
+    auto& end_act = tp.end_act;
+    auto& syncb = tp.syncb;
+    // ---- split barriers (K == 1): every phase boundary is a named barrier
+    // (ids 1..15 round robin).  A warp *syncs* on barrier p only right before it first
+    // reads a cross-warp value it has not yet synced for; otherwise it just *arrives*
+    // (bar.arrive: release, no wait) and runs on into its next phase.  Ops of a phase
+    // that need no fresh cross-warp value are hoisted ahead of those that do.
+    static const bool env_split = getenv("VSB_SPLIT") != nullptr;
+    tp.split = K == 1 && (opt.split_barriers || env_split);
+    const bool split = tp.split;
+    auto in_chunk0 = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
+    auto xwarp = [&](int32_t u, int w) { return in_chunk0(u) && warp_of[u] != w; };
+    if (split) {
+        std::vector<int32_t> late_stamp(N, -1);
+        for (int w = 0; w < W; ++w)
+            for (int ph = 1; ph < P; ++ph) {
+                auto& sq = ts.seq[w][ph];
+                std::vector<int32_t> early, late;
+                const int32_t stamp = w * (P + 1) + ph;
+                for (int32_t q : sq) {
+                    const Node& nd = p.nodes[q];
+                    bool lt = false;
+                    for (int k = 0; k < kArity[nd.op] && !lt; ++k) {
+                        const int32_t u = nd.arg[k];
+                        lt = (xwarp(u, w) && phase_of[u] >= ph - 1) || late_stamp[u] == stamp;
+                    }
+                    if (lt) { late.push_back(q); late_stamp[q] = stamp; } else early.push_back(q);
+                }
+                sq = early;
+                sq.insert(sq.end(), late.begin(), late.end());
+            }
+    }
+    // sync plan: sync_at[q] = barrier phase to bar.sync before op q; end_act[w][ph] =
+    // 0 nothing, 1 bar.arrive / 2 bar.sync on barrier ph-1 after the phase's ops;
+    // syncb[w][ph] = last barrier phase this warp synced on before phase ph's ops
+    sync_at.assign(N, -1);
+    end_act.assign(W, std::vector<int8_t>(P, 0));
+    syncb.assign(W, std::vector<int32_t>(P, -1));
+    if (split) {
+        std::vector<int32_t> seen(N, -1);
+        for (int w = 0; w < W; ++w) {
+            int last_synced = -1, pending = -1;
+            for (int ph = 0; ph < P; ++ph) {
+                syncb[w][ph] = last_synced;
+                for (int32_t q : ts.seq[w][ph]) {
+                    const Node& nd = p.nodes[q];
+                    int need = -1;
+                    for (int k = 0; k < kArity[nd.op]; ++k) {
+                        const int32_t u = nd.arg[k];
+                        if (!xwarp(u, w) || seen[u] == w) continue;
+                        seen[u] = w;
+                        need = std::max(need, phase_of[u]);
+                    }
+                    if (need > last_synced) {   // pending (= ph - 1) >= need
+                        sync_at[q] = pending;
+                        last_synced = pending;
+                        pending = -1;
+                    }
+                    seen[q] = w;
+                }
+                if (pending >= 0) {
+                    const bool force = pending - last_synced >= 12;  // ids recycle every 15 phases
+                    end_act[w][ph] = force ? 2 : 1;
+                    if (force) last_synced = pending;
+                }
+                pending = ph;
+            }
+        }
+    }
+}
+
+void Emitter::team_cross_warp_values(TeamPlan& tp, Chunk& ch, int c) {
+    auto& W = tp.W;
+    auto& Wl = tp.Wl;
+    auto& IPB = tp.IPB;
+    auto& P = tp.P;
+    auto& ts = tp.ts;
+    auto& warp_of = tp.warp_of;
+    auto& phase_of = tp.phase_of;
+    auto& extra_stores = tp.extra_stores;
+    auto& xend = tp.xend;
+    auto& xranks = tp.xranks;
+    auto& xcons = tp.xcons;
+    auto& cap = tp.cap;
+    auto& xvals = tp.xvals;
+    auto& to_global = tp.to_global;
+    const bool last = (c == C - 1);
+    ch.est_efficiency = ts.makespan > 0 ? ts.total_cost / (W * ts.makespan) : 1.0;
+    auto in_chunk = [&](int32_t u) { return tp.in_chunk(p, ch, u); };
+    // output stores not owned by an in-chunk producer: spread over warps, phase 0
+    extra_stores.assign(W, {});
+    if (last) {
+        int rr = 0;
+        for (size_t s = 0; s < p.stores.size(); ++s) {
+            const int32_t u = p.stores[s].node;
+            if (in_chunk(u)) continue;
+            extra_stores[rr++ % W].push_back(static_cast<int32_t>(s));
+        }
+    }
+    // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
+    xend.assign(N, -1);
+    xranks.assign(N, 0);  // CTA ranks (of the cluster) holding consumers
+    xcons.assign(N, {});  // consumer warp * 100000 + first-use phase
+    {
+        std::vector<int32_t> seen_stamp(N, -1);
+        for (int w = 0; w < W; ++w)
+            for (int ph = 0; ph < P; ++ph)
+                for (int32_t m : ts.seq[w][ph]) {
+                    const Node& nd = p.nodes[m];
+                    for (int k = 0; k < kArity[nd.op]; ++k) {
+                        const int32_t u = nd.arg[k];
+                        if (!in_chunk(u) || warp_of[u] == w || seen_stamp[u] == w) continue;
+                        seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
+                        xend[u] = std::max(xend[u], ph);
+                        xranks[u] |= 1u << (w / Wl);
+                        xcons[u].push_back(w * 100000 + ph);
+                    }
+                }
+    }
+    if (getenv("VSB_PAIR_STATS")) {
+        std::map<std::vector<int32_t>, int> sig;
+        int64_t nx = 0, lds = 0;
+        for (int64_t q = ch.first; q < ch.last; ++q) {
+            if (xend[q] < 0) continue;
+            std::vector<int32_t> k2 = xcons[q];
+            std::sort(k2.begin(), k2.end());
+            k2.push_back(warp_of[q]);
+            k2.push_back(phase_of[q]);
+            ++sig[k2]; ++nx; lds += static_cast<int64_t>(xcons[q].size());
+        }
+        int64_t pairs = 0, pair_lds = 0;
+        for (auto& kv : sig) { pairs += kv.second / 2; pair_lds += (kv.second / 2) * static_cast<int64_t>(kv.first.size() - 2); }
+        fprintf(stderr, "chunk %d: xfers %lld lds %lld  pairable: %lld pairs (saves %lld STS + %lld LDS)\n", c,
+                (long long)nx, (long long)lds, (long long)pairs, (long long)pairs, (long long)pair_lds);
+    }
+    // capacity: smem slots of 32 lanes; longest intervals overflow to global scratch
+    cap = std::max<int64_t>(0, opt.team_smem / (IPB * rsz));
+    xvals.clear();
+    for (int64_t q = ch.first; q < ch.last; ++q)
+        if (xend[q] >= 0) xvals.push_back(static_cast<int32_t>(q));
+    ch.xfers = static_cast<int64_t>(xvals.size());
+    to_global.assign(N, 0);
+    {
+        std::vector<int32_t> occ(P + 1, 0);
+        for (int32_t q : xvals)
+            for (int ph = phase_of[q]; ph <= xend[q]; ++ph) ++occ[ph];
+        int32_t mx = 0;
+        for (int32_t o : occ) mx = std::max(mx, o);
+        if (mx > cap) {
+            std::vector<int32_t> order = xvals;
+            std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b2) {
+                return (xend[a] - phase_of[a]) > (xend[b2] - phase_of[b2]);
+            });
+            for (int32_t q : order) {
+                int32_t m2 = 0;
+                for (int ph = phase_of[q]; ph <= xend[q]; ++ph) m2 = std::max(m2, occ[ph]);
+                if (m2 <= cap) continue;
+                to_global[q] = 1;
+                for (int ph = phase_of[q]; ph <= xend[q]; ++ph) --occ[ph];
+            }
+        }
+    }
+}
+
+void Emitter::team_rows(TeamPlan& tp, Chunk& ch) {
+    auto& W = tp.W;
+    auto& K = tp.K;
+    auto& P = tp.P;
+    auto& ts = tp.ts;
+    auto& warp_of = tp.warp_of;
+    auto& phase_of = tp.phase_of;
+    auto& xend = tp.xend;
+    auto& xcons = tp.xcons;
+    auto& cap = tp.cap;
+    auto& xvals = tp.xvals;
+    auto& to_global = tp.to_global;
+    auto& mate = tp.mate;
+    auto& second = tp.second;
+    auto& xslot = tp.xslot;
+    auto& n_smem = tp.n_smem;
+    auto& n_glob = tp.n_glob;
+    auto& syncb = tp.syncb;
+    const bool split = tp.split;
+    // paired exchange: two smem values with the same producer warp, birth phase and
+    // (consumer warp, first-use phase) set travel as one 128-bit STS/LDS; a pair
+    // occupies two slot rows laid out [row pair][lane][2]
+    mate.assign(N, -1);
+    second.assign(N, 0);
+    static const bool env_pair = getenv("VSB_PAIR") != nullptr;
+    tp.pairing = (opt.pair_xfers || env_pair) && K == 1;
+    const bool pairing = tp.pairing;
+    if (pairing) {
+        std::map<std::vector<int32_t>, int32_t> open;  // signature -> unpaired value
+        for (int w = 0; w < W; ++w)
+            for (int ph = 0; ph < P; ++ph)
+                for (int32_t q : ts.seq[w][ph]) {
+                    if (xend[q] < 0 || to_global[q]) continue;
+                    std::vector<int32_t> sig = xcons[q];
+                    static const bool relaxed = getenv("VSB_PAIR_RELAXED") != nullptr;
+                    if (relaxed) for (auto& x : sig) x /= 100000;  // consumer warps only
+                    std::sort(sig.begin(), sig.end());
+                    sig.push_back(w);
+                    sig.push_back(ph);
+                    auto it = open.find(sig);
+                    if (it == open.end()) { open.emplace(std::move(sig), q); continue; }
+                    mate[it->second] = q;
+                    mate[q] = it->second;
+                    second[q] = 1;  // defined after its mate in the producer's sequence
+                    open.erase(it);
+                }
+    }
+    xslot.assign(N, -1);   // smem row (single) / first row of the pair / global slot
+    n_smem = 0;
+    n_glob = 0;
+    auto allocate = [&]() {
+        std::fill(xslot.begin(), xslot.end(), -1);
+        std::vector<std::vector<int32_t>> born(P), dies(P);
+        for (int32_t q : xvals) {
+            if (mate[q] >= 0 && second[q]) continue;  // the pair is allocated once, by its first value
+            born[phase_of[q]].push_back(q);
+            dies[mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]].push_back(q);
+        }
+        // free rows keyed by (last read phase, row): with split barriers a row read up to
+        // phase e may be rewritten by warp w only once w has synced on barrier >= e
+        using Fr = std::pair<int32_t, int32_t>;
+        std::priority_queue<Fr, std::vector<Fr>, std::greater<Fr>> fs_free, fg_free, fp_free;
+        int32_t ns = 0, ng = 0, np = 0;
+        for (int ph = 0; ph < P; ++ph) {
+            if (ph > 0)
+                for (int32_t q : dies[ph - 1]) {
+                    const int32_t e = mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q];
+                    (to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free).push({e, xslot[q]});
+                }
+            for (int32_t q : born[ph]) {
+                auto& fq = to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free;
+                int32_t& nx = to_global[q] ? ng : mate[q] >= 0 ? np : ns;
+                const int32_t ok_upto = split ? syncb[warp_of[q]][ph] : ph - 1;
+                if (!fq.empty() && fq.top().first <= ok_upto) { xslot[q] = fq.top().second; fq.pop(); }
+                else xslot[q] = nx++;
+            }
+        }
+        // rows: singles [0, ns), pairs ns + 2 * pair index
+        for (int32_t q : xvals)
+            if (!to_global[q] && mate[q] >= 0 && !second[q]) xslot[q] = ns + 2 * xslot[q];
+        for (int32_t q : xvals)
+            if (!to_global[q] && mate[q] >= 0 && second[q]) xslot[q] = xslot[mate[q]];
+        n_smem = ns + 2 * static_cast<int64_t>(np);
+        n_glob = ng;
+        ch.pairs = np;
+    };
+    allocate();
+    if (pairing && n_smem > cap) {  // separate pair pool fragmented past the budget: unpaired
+        std::fill(mate.begin(), mate.end(), -1);
+        std::fill(second.begin(), second.end(), 0);
+        allocate();
+    }
+    // still over the smem budget (separate pair pool, or rows held back for split-barrier WAR
+    // safety): demote the longest-lived smem values to global scratch until it fits
+    for (int iter = 0; n_smem > cap && iter < 64; ++iter) {
+        std::vector<int32_t> cand;
+        for (int32_t q : xvals)
+            if (!to_global[q] && !(mate[q] >= 0 && second[q])) cand.push_back(q);
+        if (cand.empty()) break;
+        auto life = [&](int32_t q) { return (mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]) - phase_of[q]; };
+        std::sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b2) { return life(a) > life(b2); });
+        const size_t k = std::max<size_t>(1, static_cast<size_t>(cand.size() * std::min(0.5, 0.02 + double(n_smem - cap) / double(n_smem))));
+        for (size_t i = 0; i < k && i < cand.size(); ++i) {
+            const int32_t q = cand[i];
+            to_global[q] = 1;
+            if (mate[q] >= 0) {
+                to_global[mate[q]] = 1;
+                second[mate[q]] = 0;
+                mate[mate[q]] = -1;
+                mate[q] = -1;
+            }
+        }
+        allocate();
+    }
+}
+
+void Emitter::team_live_stats(TeamPlan& tp, int c) {
+    auto& W = tp.W;
+    auto& P = tp.P;
+    auto& ts = tp.ts;
+    auto& xend = tp.xend;
+    {
+        // per-warp register live set: values defined by or loaded into warp w, live from
+        // definition/first load to their last use in w (stores count as uses)
+        int64_t worst = 0, sum_peak = 0;
+        for (int w = 0; w < W; ++w) {
+            std::vector<int64_t> first(N, -1), lastu(N, -1);
+            int64_t pos = 0;
+            for (int ph = 0; ph < P; ++ph)
+                for (int32_t q : ts.seq[w][ph]) {
+                    const Node& nd = p.nodes[q];
+                    for (int k = 0; k < kArity[nd.op]; ++k) {
+                        const int32_t u = nd.arg[k];
+                        if (p.nodes[u].op == OP_CONST) continue;
+                        if (first[u] < 0) first[u] = pos;
+                        lastu[u] = pos;
+                    }
+                    first[q] = pos;
+                    if (lastu[q] < pos) lastu[q] = pos;
+                    if (xend[q] >= 0 || slot_of[q] >= 0 || !stores_of[q].empty()) lastu[q] = std::max(lastu[q], pos + 1);
+                    ++pos;
+                }
+            std::vector<int64_t> delta(pos + 2, 0);
+            for (int64_t q = 0; q < N; ++q)
+                if (first[q] >= 0) { delta[first[q]] += 1; delta[lastu[q] + 1] -= 1; }
+            int64_t run = 0, peak = 0;
+            for (int64_t i = 0; i <= pos; ++i) { run += delta[i]; peak = std::max(peak, run); }
+            worst = std::max(worst, peak);
+            sum_peak += peak;
+        }
+        if (getenv("VSB_LIVE_STATS"))
+            fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
+                    double(sum_peak) / W);
+        ks.live_total = std::max(ks.live_total, sum_peak);  // ~ doubles per instance held in registers
+    }
+}
+
+void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
+    const bool last = (c == C - 1);
+    const std::string& nbuf_s = ch.name;
+    const char* nbuf = nbuf_s.c_str();
+    auto in_chunk = [&](int32_t u) { return tp.in_chunk(p, ch, u); };
+    auto& W = tp.W;
+    auto& K = tp.K;
+    auto& Wl = tp.Wl;
+    auto& IPB = tp.IPB;
+    auto& P = tp.P;
+    auto& ts = tp.ts;
+    auto& warp_of = tp.warp_of;
+    auto& sync_at = tp.sync_at;
+    auto& end_act = tp.end_act;
+    auto& extra_stores = tp.extra_stores;
+    auto& xend = tp.xend;
+    auto& xranks = tp.xranks;
+    auto& to_global = tp.to_global;
+    auto& mate = tp.mate;
+    auto& second = tp.second;
+    auto& xslot = tp.xslot;
+    auto& n_smem = tp.n_smem;
+    auto& n_glob = tp.n_glob;
+    const bool split = tp.split;
+    ch.smem_slots = n_smem;
+    ch.overflow_slots = n_glob;
+    max_overflow = std::max(max_overflow, n_glob);
+    ch.smem_bytes = n_smem * IPB * rsz;
+
+    if (K > 1)
+        b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", K, nbuf);
+    else
+        b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
+    b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
+    b.put("    const int lane = threadIdx.x & 31;\n");
+    b.put("    const int wid = threadIdx.x >> 5;\n");
+    b.put("    const int grp = wid / %d;\n", Wl);
+    if (K > 1) {
+        b.put("    const int crank = (int)(blockIdx.x %% %d);\n", K);
+        b.put("    const long long cid = (long long)(blockIdx.x / %d);\n", K);
+    } else {
+        b.put("    const int crank = 0;\n");
+        b.put("    const long long cid = (long long)blockIdx.x;\n");
+    }
+    b.put("    const int warp = crank * %d + wid %% %d;\n", Wl, Wl);
+    // A.ipc <= VS_IPB instances per cluster (the runtime shrinks it so that the
+    // grid fills whole waves of SMs; the spare lanes idle)
+    // spare lanes mirror the last instance (identical bits; benign duplicate stores)
+    b.put("    long long t = cid * A.ipc + grp * 32 + lane;\n");
+    b.put("    if (grp * 32 + lane >= A.ipc || t >= A.n) t = A.n - 1;\n");
+    b.put("    const long long e = A.e0 + t;\n");
+    b.put("    (void)e;\n");
+    io_bases(b);
+    b.put("    real* __restrict__ S = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32 + lane;\n");
+    b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");
+    b.put("    real* __restrict__ X2 = vs_smem + (grp * 32 + lane) * 2;   // paired rows [row][lane][2]\n");
+    b.put("    (void)S; (void)X; (void)X2;\n");
+    if (K > 1) {
+        // shared::cluster addresses of this lane's X column in every CTA of the cluster
+        b.put("    const unsigned xl = (unsigned)__cvta_generic_to_shared(X);\n");
+        for (int r = 0; r < K; ++r)
+            b.put("    unsigned XR%d; asm(\"mapa.shared::cluster.u32 %%0, %%1, %d;\" : \"=r\"(XR%d) : \"r\"(xl)); (void)XR%d;\n",
+                  r, r, r, r);
+        // every CTA of the cluster must be running before the first DSMEM store
+        b.put("    VS_CBAR();\n");
+    }
+    b.put("    switch (warp) {\n");
+    std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
+    for (int w = 0; w < W; ++w) {
+        b.put("    case %d: {\n", w);
+        const char* ind = "        ";
+        auto ensure = [&](int32_t u) {
+            const Node& nu = p.nodes[u];
+            if (nu.op == OP_CONST || have[u] == w) return;
+            have[u] = w;
+            if (nu.op == OP_INPUT) { input_load(b, u, ind); return; }
+            if (!in_chunk(u)) {  // imported from an earlier chunk
+                b.put("%sconst real v%d = S[%d * VS_IPB];\n", ind, u, slot_of[u]);
+                ++ch.loads;
+                return;
+            }
+            // produced by another warp in an earlier phase
+            if (to_global[u]) {
+                b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
+            } else if (mate[u] >= 0) {
+                const int32_t a0 = second[u] ? mate[u] : u, a1 = second[u] ? u : mate[u];
+                b.put("%sconst vec2_t p%d = *reinterpret_cast<const vec2_t*>(X2 + %d * VS_IPB);\n", ind, a0, xslot[u]);
+                b.put("%sconst real v%d = p%d.x, v%d = p%d.y;\n", ind, a0, a0, a1, a0);
+                have[mate[u]] = w;
+            } else {
+                b.put("%sconst real v%d = X[%d * VS_IPB];\n", ind, u, xslot[u]);
+            }
+        };
+        for (int32_t s : extra_stores[w]) {
+            const int32_t u = p.stores[s].node;
+            ensure(u);
+            emit_store(b, s, opnd(u), ind, false);
+        }
+        for (int ph = 0; ph < P; ++ph) {
+            for (int32_t q : ts.seq[w][ph]) {
+                const Node& nd = p.nodes[q];
+                if (sync_at[q] >= 0) b.put("%sVS_BSYNC(%d);\n", ind, 1 + sync_at[q] % 15);
+                for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+                if (partner[q] >= 0 && warp_of[partner[q]] != w) {
+                    // mate lives on another warp: no pairing
+                    b.put("%sconst real v%d = %s;\n", ind, q, expr_of(nd).c_str());
+                    done[q] = 1;
+                } else {
+                    emit_def(b, q, done, ind);
+                }
+                have[q] = w;
+                if (xend[q] >= 0) {
+                    if (to_global[q]) {
+                        b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
+                    } else {
+                        const int my = w / Wl;
+                        if (mate[q] >= 0) {
+                            if (second[q])  // both defined now: one 128-bit store
+                                b.put("%s*reinterpret_cast<vec2_t*>(X2 + %d * VS_IPB) = vec2_t{v%d, v%d};\n", ind,
+                                      xslot[q], mate[q], q);
+                        } else if (xranks[q] & (1u << my)) {
+                            b.put("%sX[%d * VS_IPB] = v%d;\n", ind, xslot[q], q);
+                        }
+                        for (int r = 0; r < K; ++r) {
+                            if (r == my || !(xranks[q] & (1u << r))) continue;
+                            b.put("%sasm volatile(\"st.shared::cluster.%s [%%0+%" PRId64 "], %%1;\" :: \"r\"(XR%d), \"%s\"(v%d));\n",
+                                  ind, f32 ? "f32" : "f64", static_cast<int64_t>(xslot[q]) * IPB * rsz, r, f32 ? "f" : "d", q);
+                            ++ch.remote_stores;
+                        }
+                    }
+                }
+                if (slot_of[q] >= 0) { b.put("%sS[%d * VS_IPB] = v%d;\n", ind, slot_of[q], q); ++ch.stores; }
+                if (last)
+                    for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
+            }
+            if (split) {
+                if (end_act[w][ph]) b.put(end_act[w][ph] == 2 ? "%sVS_BSYNC(%d);\n" : "%sVS_BARV(%d);\n", ind,
+                                          1 + (ph - 1) % 15);
+            } else if (ph + 1 < P) {
+                b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
+            }
+        }
+        b.put("        break;\n    }\n");
+    }
+    b.put("    }\n}\n");
+}
+
+Kernelset Emitter::run() {
+    ks.block = opt.block;
+    ks.f32 = opt.f32;
+    ks.layout = opt.layout;
+    team = opt.team >= 2;
+    ks.team = team ? opt.team : 0;
+    N = static_cast<int64_t>(p.nodes.size());
+    n_in = static_cast<int>(p.nnz_in.size());
+    n_out = static_cast<int>(p.nnz_out.size());
+    f32 = opt.f32;
+    rsz = f32 ? 4 : 8;
+    real = f32 ? "float" : "double";
+    fs = f32 ? "f" : "";
+    soa = opt.layout == Layout::SOA;
+    cut_chunks();
+    plan_cross_chunk();
+    trig_exact = opt.exact_trig && !f32;
+    plan_staging();
+    build_header();
+    loaded_in.assign(N, -1);  // thread mode: chunk in which a value is available
+    done.assign(N, 0);
     for (int c = 0; c < C; ++c) {
         Chunk ch;
         ch.first = cuts[c];
         ch.last = cuts[c + 1];
         ch.ops = opcum[ch.last] - opcum[ch.first];
-        const bool first = (c == 0), last = (c == C - 1);
         char nbuf[96];
         snprintf(nbuf, sizeof nbuf, "vsk_%s_c%d", tag.c_str(), c);
         ch.name = nbuf;
         Out b;
-
-        auto emit_store = [&](Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) {
-            const Store& s = p.stores[s_idx];
-            if (staged) {
-                o.put("%sorow[%" PRId64 "] = %s;\n", ind, p.out_base[s.j] + s.k, val.c_str());
-            } else if (soa) {
-                o.put("%sO%d[(long long)%d * A.io_ld] = %s;\n", ind, s.j, s.k, val.c_str());
-            } else {
-                o.put("%sO%d[%d] = %s;\n", ind, s.j, s.k, val.c_str());  // immediate offset
-            }
-        };
-        auto input_load = [&](Out& o, int32_t u, const char* ind) {
-            const Node& nu = p.nodes[u];
-            if (soa)
-                o.put("%sconst real v%d = __ldg(I%d + (long long)%d * A.io_ld);\n", ind, u, nu.in_i, nu.in_k);
-            else
-                o.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
-        };
-        // per-thread base pointers of every input/output row (hoisted address math)
-        auto io_bases = [&](Out& o) {
-            for (int i = 0; i < n_in; ++i)
-                o.put(soa ? "    const real* __restrict__ I%d = A.in[%d] + e;\n"
-                          : "    const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n",
-                      i, i, p.nnz_in[i]);
-            for (int j = 0; j < n_out; ++j)
-                o.put(soa ? "    real* __restrict__ O%d = A.out[%d] + e;\n"
-                          : "    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n",
-                      j, j, p.nnz_out[j]);
-            for (int i = 0; i < n_in; ++i) o.put("    (void)I%d;\n", i);
-            for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
-        };
-
-        if (!team) {
-            // ================= one thread per instance =================
-            ch.stage_in = first && stage_in;
-            ch.stage_out = last && stage_out;
-            ch.threads = opt.block;
-            ch.inst_per_block = opt.block;
-            const int64_t sin_off = 0;
-            const int64_t sout_off = ch.stage_in ? SI * opt.block : 0;
-            ch.smem_bytes = (ch.stage_in ? in_bytes : 0) + (ch.stage_out ? out_bytes : 0);
-            b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
-            b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
-            // spare threads of the last block mirror the last instance: same inputs, same
-            // bits, so their (duplicate) stores are benign and no load/store needs a guard
-            b.put("    long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
-            b.put("    if (t >= A.n) t = A.n - 1;\n");
-            b.put("    const long long e = A.e0 + t;\n");
-            b.put("    (void)e;\n");
-            io_bases(b);
-            // block-local SoA scratch [block][slot][VS_IPB]: slot offsets are immediates
-            if (ks.scratch_slots > 0)
-                b.put("    real* __restrict__ S = A.scratch + (long long)blockIdx.x * (VS_NSLOT * VS_IPB) + threadIdx.x;\n");
-            if (ch.stage_in || ch.stage_out) {
-                b.put("    const long long blk0 = (long long)blockIdx.x * VS_BS;\n");
-                b.put("    const int nblk = (int)((A.n - blk0) < VS_BS ? (A.n - blk0) : VS_BS);\n");
-            }
-            if (ch.stage_in) {
-                for (int i = 0; i < n_in; ++i) {
-                    if (p.nnz_in[i] == 0) continue;
-                    b.put("    vs_stage_in<%" PRId64 ", %" PRId64 ", %" PRId64 ">(vs_smem + %" PRId64 ", A.in[%d] + (A.e0 + blk0) * %" PRId64 "LL, nblk * %" PRId64 ");\n",
-                          p.nnz_in[i], p.in_base[i], SI, sin_off, i, p.nnz_in[i], p.nnz_in[i]);
-                }
-                b.put("    __syncthreads();\n");
-                // spare threads of the last block read the last staged row (they mirror instance n-1,
-                // whose outputs they may store when outputs are not staged)
-                b.put("    const real* __restrict__ srow = vs_smem + %" PRId64 " + (threadIdx.x < nblk ? threadIdx.x : nblk - 1) * %" PRId64 ";\n", sin_off, SI);
-            }
-            if (ch.stage_out) b.put("    real* __restrict__ orow = vs_smem + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", sout_off, SO);
-
-            std::function<void(int32_t)> ensure = [&](int32_t u) {
-                const Node& nu = p.nodes[u];
-                if (nu.op == OP_CONST || loaded_in[u] == c) return;
-                loaded_in[u] = c;
-                if (def_chunk[u] < c || (nu.op == OP_INPUT && !first)) {
-                    b.put("    const real v%d = S[%d * VS_IPB];\n", u, slot_of[u]);
-                    ++ch.loads;
-                    return;
-                }
-                if (ch.stage_in) b.put("    const real v%d = srow[%" PRId64 "];\n", u, p.in_base[nu.in_i] + nu.in_k);
-                else input_load(b, u, "    ");
-                if (slot_of[u] >= 0 && first) { b.put("    S[%d * VS_IPB] = v%d;\n", slot_of[u], u); ++ch.stores; }
-            };
-            if (first)
-                for (int64_t q = 0; q < N; ++q)
-                    if (p.nodes[q].op == OP_INPUT && slot_of[q] >= 0) ensure(static_cast<int32_t>(q));
-            if (last) {
-                for (size_t s = 0; s < p.stores.size(); ++s) {
-                    const int32_t u = p.stores[s].node;
-                    const Node& nu = p.nodes[u];
-                    if (nu.op > OP_INPUT && def_chunk[u] == c) continue;
-                    ensure(u);
-                    emit_store(b, static_cast<int32_t>(s), opnd(u), "    ", ch.stage_out);
-                }
-            }
-            for (int64_t q = ch.first; q < ch.last; ++q) {
-                const Node& nd = p.nodes[q];
-                if (nd.op <= OP_ASSIGN) continue;
-                for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
-                emit_def(b, q, done, "    ");
-                loaded_in[q] = c;
-                if (slot_of[q] >= 0) { b.put("    S[%d * VS_IPB] = v%" PRId64 ";\n", slot_of[q], q); ++ch.stores; }
-                if (last)
-                    for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), "    ", ch.stage_out);
-            }
-            if (ch.stage_out) {
-                b.put("    __syncthreads();\n");
-                for (int j = 0; j < n_out; ++j) {
-                    if (p.nnz_out[j] == 0) continue;
-                    b.put("    vs_stage_out<%" PRId64 ", %" PRId64 ", %" PRId64 ">(A.out[%d] + (A.e0 + blk0) * %" PRId64 "LL, vs_smem + %" PRId64 ", nblk * %" PRId64 ");\n",
-                          p.nnz_out[j], p.out_base[j], SO, j, p.nnz_out[j], sout_off, p.nnz_out[j]);
-                }
-            }
-            b.put("}\n");
-            // ---- persistent TMA variant: full 128-instance tiles stream through two smem
-            // buffers with cp.async.bulk (one bulk copy per input / output array, completion on
-            // an mbarrier), the next tiles' loads in flight while the current tile computes
-            const bool tma = opt.bulk_io && same_kernel && !soa && ni_tot > 0 && no_tot > 0 &&
-                             2 * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
-            if (tma) {
-                ch.tma = true;
-                const int64_t IT = ni_tot * opt.block, OT = no_tot * opt.block;  // tile sizes (elements)
-                ch.tma_smem_bytes = 2 * (IT + OT) * rsz + 16;
-                b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_tma(const VsArgs A) {\n", opt.min_blocks, nbuf);
-                b.put("    extern __shared__ __align__(128) real vs_smem[];\n");
-                b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", 2 * (IT + OT));
-                b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the partial tail is done after the loop\n");
-                b.put("    if (threadIdx.x == 0) { vs_mbar_init(mbar, 1); vs_mbar_init(mbar + 1, 1); VS_FENCE_MBAR_INIT(); }\n");
-                b.put("    __syncthreads();\n");
-                // loads of one tile into buffer bs
-                Out ld;
-                ld.put("    auto issue = [&](long long tile, int bs) {\n");
-                ld.put("        real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
-                ld.put("        const long long e = A.e0 + tile * VS_BS;\n");
-                ld.put("        vs_mbar_expect(mbar + bs, %" PRId64 "u);\n", IT * rsz);
-                for (int i = 0; i < n_in; ++i) {
-                    if (p.nnz_in[i] == 0) continue;
-                    ld.put("        vs_bulk_load(ib + %" PRId64 ", A.in[%d] + e * %" PRId64 "LL, %" PRId64 "u, mbar + bs);\n",
-                           p.in_base[i] * opt.block, i, p.nnz_in[i], p.nnz_in[i] * opt.block * rsz);
-                }
-                ld.put("    };\n");
-                b.s += ld.s;
-                b.put("    long long tile = blockIdx.x;\n");
-                b.put("    if (threadIdx.x == 0) {\n");
-                b.put("        if (tile < ntiles) issue(tile, 0);\n");
-                b.put("        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);\n");
-                b.put("    }\n");
-                b.put("    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {\n");
-                b.put("        const int bs = k & 1;\n");
-                b.put("        vs_mbar_wait(mbar + bs, (k >> 1) & 1);\n");
-                b.put("        if (threadIdx.x == 0 && k >= 2) VS_BULK_WAIT_READ1();  // out buffer bs free again\n");
-                b.put("        __syncthreads();\n");
-                b.put("        const real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
-                b.put("        real* ob = vs_smem + %" PRId64 " + bs * %" PRId64 ";\n", 2 * IT, OT);
-                for (int i = 0; i < n_in; ++i)
-                    b.put("        const real* __restrict__ I%d = ib + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", i,
-                          p.in_base[i] * opt.block, p.nnz_in[i]);
-                for (int j = 0; j < n_out; ++j)
-                    b.put("        real* __restrict__ O%d = ob + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", j,
-                          p.out_base[j] * opt.block, p.nnz_out[j]);
-                for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
-                for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
-                // body: same op sequence, inputs from the smem tile row, outputs to the smem out row
-                std::vector<uint8_t> done2(N, 0), got(N, 0);
-                const char* ind2 = "        ";
-                auto ensure2 = [&](int32_t u) {
-                    const Node& nu = p.nodes[u];
-                    if (nu.op != OP_INPUT || got[u]) return;
-                    got[u] = 1;
-                    b.put("%sconst real v%d = I%d[%d];\n", ind2, u, nu.in_i, nu.in_k);
-                };
-                for (size_t si = 0; si < p.stores.size(); ++si) {
-                    const int32_t u = p.stores[si].node;
-                    if (p.nodes[u].op > OP_INPUT) continue;
-                    ensure2(u);
-                    b.put("%sO%d[%d] = %s;\n", ind2, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
-                }
-                for (int64_t q = ch.first; q < ch.last; ++q) {
-                    const Node& nd = p.nodes[q];
-                    if (nd.op <= OP_ASSIGN) continue;
-                    for (int k = 0; k < kArity[nd.op]; ++k) ensure2(nd.arg[k]);
-                    emit_def(b, q, done2, ind2);
-                    for (int32_t si : stores_of[q])
-                        b.put("%sO%d[%d] = v%" PRId64 ";\n", ind2, p.stores[si].j, p.stores[si].k, q);
-                }
-                b.put("        VS_FENCE_ASYNC();   // generic-proxy smem writes -> visible to the bulk store\n");
-                b.put("        __syncthreads();\n");
-                b.put("        if (threadIdx.x == 0) {\n");
-                b.put("            const long long e = A.e0 + tile * VS_BS;\n");
-                for (int j = 0; j < n_out; ++j) {
-                    if (p.nnz_out[j] == 0) continue;
-                    b.put("            vs_bulk_store(A.out[%d] + e * %" PRId64 "LL, ob + %" PRId64 ", %" PRId64 "u);\n", j,
-                          p.nnz_out[j], p.out_base[j] * opt.block, p.nnz_out[j] * opt.block * rsz);
-                }
-                b.put("            VS_BULK_COMMIT();\n");
-                b.put("            if (tile + 2 * (long long)gridDim.x < ntiles) issue(tile + 2 * (long long)gridDim.x, bs);\n");
-                b.put("        }\n");
-                b.put("    }\n");
-                // the partial last tile (< 128 instances): one CTA, direct global loads/stores;
-                // spare threads mirror the last instance (benign duplicate stores)
-                b.put("    if (A.n %% VS_BS != 0 && blockIdx.x == (unsigned)(ntiles %% gridDim.x)) {\n");
-                b.put("        long long t = ntiles * VS_BS + threadIdx.x;\n");
-                b.put("        if (t >= A.n) t = A.n - 1;\n");
-                b.put("        const long long e = A.e0 + t;\n");
-                for (int i = 0; i < n_in; ++i)
-                    b.put("        const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n", i, i, p.nnz_in[i]);
-                for (int j = 0; j < n_out; ++j)
-                    b.put("        real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
-                for (int i = 0; i < n_in; ++i) b.put("        (void)I%d;\n", i);
-                for (int j = 0; j < n_out; ++j) b.put("        (void)O%d;\n", j);
-                {
-                    std::vector<uint8_t> done3(N, 0), got3(N, 0);
-                    auto ensure3 = [&](int32_t u) {
-                        const Node& nu = p.nodes[u];
-                        if (nu.op != OP_INPUT || got3[u]) return;
-                        got3[u] = 1;
-                        b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind2, u, nu.in_i, nu.in_k);
-                    };
-                    for (size_t si = 0; si < p.stores.size(); ++si) {
-                        const int32_t u = p.stores[si].node;
-                        if (p.nodes[u].op > OP_INPUT) continue;
-                        ensure3(u);
-                        b.put("%sO%d[%d] = %s;\n", ind2, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
-                    }
-                    for (int64_t q = ch.first; q < ch.last; ++q) {
-                        const Node& nd = p.nodes[q];
-                        if (nd.op <= OP_ASSIGN) continue;
-                        for (int k = 0; k < kArity[nd.op]; ++k) ensure3(nd.arg[k]);
-                        emit_def(b, q, done3, ind2);
-                        for (int32_t si : stores_of[q])
-                            b.put("%sO%d[%d] = v%" PRId64 ";\n", ind2, p.stores[si].j, p.stores[si].k, q);
-                    }
-                }
-                b.put("    }\n");
-                b.put("    if (threadIdx.x == 0) VS_BULK_WAIT_ALL();\n");
-                b.put("}\n");
-            }
-        } else {
-            // ================= team mode: W warps x 32 instances =================
-            const int W = opt.team, K = TK, G = TG, Wl = TWl;
-            ch.threads = Wl * G * 32;
-            ch.inst_per_block = 32 * G;
-            ch.cluster = K;
-            const int IPB = 32 * G;
-            std::vector<int32_t> warp_of(N, -1), phase_of(N, -1);
-            TeamSchedule ts = schedule_team(p, ch.first, ch.last, W, std::max(1, opt.phase_cost), opt.priority,
-                                            K > 1 ? Wl : 0, warp_of, phase_of);
-            const int P = ts.P;
-            ch.phases = P;
-            // ---- split barriers (K == 1): every phase boundary is a named barrier
-            // (ids 1..15 round robin).  A warp *syncs* on barrier p only right before it first
-            // reads a cross-warp value it has not yet synced for; otherwise it just *arrives*
-            // (bar.arrive: release, no wait) and runs on into its next phase.  Ops of a phase
-            // that need no fresh cross-warp value are hoisted ahead of those that do.
-            static const bool env_split = getenv("VSB_SPLIT") != nullptr;
-            const bool split = K == 1 && (opt.split_barriers || env_split);
-            auto in_chunk0 = [&](int32_t u) { return u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN; };
-            auto xwarp = [&](int32_t u, int w) { return in_chunk0(u) && warp_of[u] != w; };
-            if (split) {
-                std::vector<int32_t> late_stamp(N, -1);
-                for (int w = 0; w < W; ++w)
-                    for (int ph = 1; ph < P; ++ph) {
-                        auto& sq = ts.seq[w][ph];
-                        std::vector<int32_t> early, late;
-                        const int32_t stamp = w * (P + 1) + ph;
-                        for (int32_t q : sq) {
-                            const Node& nd = p.nodes[q];
-                            bool lt = false;
-                            for (int k = 0; k < kArity[nd.op] && !lt; ++k) {
-                                const int32_t u = nd.arg[k];
-                                lt = (xwarp(u, w) && phase_of[u] >= ph - 1) || late_stamp[u] == stamp;
-                            }
-                            if (lt) { late.push_back(q); late_stamp[q] = stamp; } else early.push_back(q);
-                        }
-                        sq = early;
-                        sq.insert(sq.end(), late.begin(), late.end());
-                    }
-            }
-            // sync plan: sync_at[q] = barrier phase to bar.sync before op q; end_act[w][ph] =
-            // 0 nothing, 1 bar.arrive / 2 bar.sync on barrier ph-1 after the phase's ops;
-            // syncb[w][ph] = last barrier phase this warp synced on before phase ph's ops
-            std::vector<int32_t> sync_at(N, -1);
-            std::vector<std::vector<int8_t>> end_act(W, std::vector<int8_t>(P, 0));
-            std::vector<std::vector<int32_t>> syncb(W, std::vector<int32_t>(P, -1));
-            if (split) {
-                std::vector<int32_t> seen(N, -1);
-                for (int w = 0; w < W; ++w) {
-                    int last_synced = -1, pending = -1;
-                    for (int ph = 0; ph < P; ++ph) {
-                        syncb[w][ph] = last_synced;
-                        for (int32_t q : ts.seq[w][ph]) {
-                            const Node& nd = p.nodes[q];
-                            int need = -1;
-                            for (int k = 0; k < kArity[nd.op]; ++k) {
-                                const int32_t u = nd.arg[k];
-                                if (!xwarp(u, w) || seen[u] == w) continue;
-                                seen[u] = w;
-                                need = std::max(need, phase_of[u]);
-                            }
-                            if (need > last_synced) {   // pending (= ph - 1) >= need
-                                sync_at[q] = pending;
-                                last_synced = pending;
-                                pending = -1;
-                            }
-                            seen[q] = w;
-                        }
-                        if (pending >= 0) {
-                            const bool force = pending - last_synced >= 12;  // ids recycle every 15 phases
-                            end_act[w][ph] = force ? 2 : 1;
-                            if (force) last_synced = pending;
-                        }
-                        pending = ph;
-                    }
-                }
-            }
-            ch.est_efficiency = ts.makespan > 0 ? ts.total_cost / (W * ts.makespan) : 1.0;
-            auto in_chunk = in_chunk0;
-            // output stores not owned by an in-chunk producer: spread over warps, phase 0
-            std::vector<std::vector<int32_t>> extra_stores(W);
-            if (last) {
-                int rr = 0;
-                for (size_t s = 0; s < p.stores.size(); ++s) {
-                    const int32_t u = p.stores[s].node;
-                    if (in_chunk(u)) continue;
-                    extra_stores[rr++ % W].push_back(static_cast<int32_t>(s));
-                }
-            }
-            // cross-warp values: interval [producer phase, last first-use phase among consumer warps]
-            std::vector<int32_t> xend(N, -1);
-            std::vector<uint32_t> xranks(N, 0);  // CTA ranks (of the cluster) holding consumers
-            std::vector<std::vector<int32_t>> xcons(N);  // consumer warp * 100000 + first-use phase
-            {
-                std::vector<int32_t> seen_stamp(N, -1);
-                for (int w = 0; w < W; ++w)
-                    for (int ph = 0; ph < P; ++ph)
-                        for (int32_t m : ts.seq[w][ph]) {
-                            const Node& nd = p.nodes[m];
-                            for (int k = 0; k < kArity[nd.op]; ++k) {
-                                const int32_t u = nd.arg[k];
-                                if (!in_chunk(u) || warp_of[u] == w || seen_stamp[u] == w) continue;
-                                seen_stamp[u] = w;  // first use of u in warp w (phases ascend)
-                                xend[u] = std::max(xend[u], ph);
-                                xranks[u] |= 1u << (w / Wl);
-                                xcons[u].push_back(w * 100000 + ph);
-                            }
-                        }
-            }
-            if (getenv("VSB_PAIR_STATS")) {
-                std::map<std::vector<int32_t>, int> sig;
-                int64_t nx = 0, lds = 0;
-                for (int64_t q = ch.first; q < ch.last; ++q) {
-                    if (xend[q] < 0) continue;
-                    std::vector<int32_t> k2 = xcons[q];
-                    std::sort(k2.begin(), k2.end());
-                    k2.push_back(warp_of[q]);
-                    k2.push_back(phase_of[q]);
-                    ++sig[k2]; ++nx; lds += static_cast<int64_t>(xcons[q].size());
-                }
-                int64_t pairs = 0, pair_lds = 0;
-                for (auto& kv : sig) { pairs += kv.second / 2; pair_lds += (kv.second / 2) * static_cast<int64_t>(kv.first.size() - 2); }
-                fprintf(stderr, "chunk %d: xfers %lld lds %lld  pairable: %lld pairs (saves %lld STS + %lld LDS)\n", c,
-                        (long long)nx, (long long)lds, (long long)pairs, (long long)pairs, (long long)pair_lds);
-            }
-            // capacity: smem slots of 32 lanes; longest intervals overflow to global scratch
-            const int64_t cap = std::max<int64_t>(0, opt.team_smem / (IPB * rsz));
-            std::vector<int32_t> xvals;
-            for (int64_t q = ch.first; q < ch.last; ++q)
-                if (xend[q] >= 0) xvals.push_back(static_cast<int32_t>(q));
-            ch.xfers = static_cast<int64_t>(xvals.size());
-            std::vector<uint8_t> to_global(N, 0);
-            {
-                std::vector<int32_t> occ(P + 1, 0);
-                for (int32_t q : xvals)
-                    for (int ph = phase_of[q]; ph <= xend[q]; ++ph) ++occ[ph];
-                int32_t mx = 0;
-                for (int32_t o : occ) mx = std::max(mx, o);
-                if (mx > cap) {
-                    std::vector<int32_t> order = xvals;
-                    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b2) {
-                        return (xend[a] - phase_of[a]) > (xend[b2] - phase_of[b2]);
-                    });
-                    for (int32_t q : order) {
-                        int32_t m2 = 0;
-                        for (int ph = phase_of[q]; ph <= xend[q]; ++ph) m2 = std::max(m2, occ[ph]);
-                        if (m2 <= cap) continue;
-                        to_global[q] = 1;
-                        for (int ph = phase_of[q]; ph <= xend[q]; ++ph) --occ[ph];
-                    }
-                }
-            }
-            // paired exchange: two smem values with the same producer warp, birth phase and
-            // (consumer warp, first-use phase) set travel as one 128-bit STS/LDS; a pair
-            // occupies two slot rows laid out [row pair][lane][2]
-            std::vector<int32_t> mate(N, -1);
-            std::vector<uint8_t> second(N, 0);
-            static const bool env_pair = getenv("VSB_PAIR") != nullptr;
-            const bool pairing = (opt.pair_xfers || env_pair) && K == 1;
-            if (pairing) {
-                std::map<std::vector<int32_t>, int32_t> open;  // signature -> unpaired value
-                for (int w = 0; w < W; ++w)
-                    for (int ph = 0; ph < P; ++ph)
-                        for (int32_t q : ts.seq[w][ph]) {
-                            if (xend[q] < 0 || to_global[q]) continue;
-                            std::vector<int32_t> sig = xcons[q];
-                            static const bool relaxed = getenv("VSB_PAIR_RELAXED") != nullptr;
-                            if (relaxed) for (auto& x : sig) x /= 100000;  // consumer warps only
-                            std::sort(sig.begin(), sig.end());
-                            sig.push_back(w);
-                            sig.push_back(ph);
-                            auto it = open.find(sig);
-                            if (it == open.end()) { open.emplace(std::move(sig), q); continue; }
-                            mate[it->second] = q;
-                            mate[q] = it->second;
-                            second[q] = 1;  // defined after its mate in the producer's sequence
-                            open.erase(it);
-                        }
-            }
-            std::vector<int32_t> xslot(N, -1);   // smem row (single) / first row of the pair / global slot
-            int64_t n_smem = 0, n_glob = 0;
-            auto allocate = [&]() {
-                std::fill(xslot.begin(), xslot.end(), -1);
-                std::vector<std::vector<int32_t>> born(P), dies(P);
-                for (int32_t q : xvals) {
-                    if (mate[q] >= 0 && second[q]) continue;  // the pair is allocated once, by its first value
-                    born[phase_of[q]].push_back(q);
-                    dies[mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]].push_back(q);
-                }
-                // free rows keyed by (last read phase, row): with split barriers a row read up to
-                // phase e may be rewritten by warp w only once w has synced on barrier >= e
-                using Fr = std::pair<int32_t, int32_t>;
-                std::priority_queue<Fr, std::vector<Fr>, std::greater<Fr>> fs_free, fg_free, fp_free;
-                int32_t ns = 0, ng = 0, np = 0;
-                for (int ph = 0; ph < P; ++ph) {
-                    if (ph > 0)
-                        for (int32_t q : dies[ph - 1]) {
-                            const int32_t e = mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q];
-                            (to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free).push({e, xslot[q]});
-                        }
-                    for (int32_t q : born[ph]) {
-                        auto& fq = to_global[q] ? fg_free : mate[q] >= 0 ? fp_free : fs_free;
-                        int32_t& nx = to_global[q] ? ng : mate[q] >= 0 ? np : ns;
-                        const int32_t ok_upto = split ? syncb[warp_of[q]][ph] : ph - 1;
-                        if (!fq.empty() && fq.top().first <= ok_upto) { xslot[q] = fq.top().second; fq.pop(); }
-                        else xslot[q] = nx++;
-                    }
-                }
-                // rows: singles [0, ns), pairs ns + 2 * pair index
-                for (int32_t q : xvals)
-                    if (!to_global[q] && mate[q] >= 0 && !second[q]) xslot[q] = ns + 2 * xslot[q];
-                for (int32_t q : xvals)
-                    if (!to_global[q] && mate[q] >= 0 && second[q]) xslot[q] = xslot[mate[q]];
-                n_smem = ns + 2 * static_cast<int64_t>(np);
-                n_glob = ng;
-                ch.pairs = np;
-            };
-            allocate();
-            if (pairing && n_smem > cap) {  // separate pair pool fragmented past the budget: unpaired
-                std::fill(mate.begin(), mate.end(), -1);
-                std::fill(second.begin(), second.end(), 0);
-                allocate();
-            }
-            // still over the smem budget (separate pair pool, or rows held back for split-barrier WAR
-            // safety): demote the longest-lived smem values to global scratch until it fits
-            for (int iter = 0; n_smem > cap && iter < 64; ++iter) {
-                std::vector<int32_t> cand;
-                for (int32_t q : xvals)
-                    if (!to_global[q] && !(mate[q] >= 0 && second[q])) cand.push_back(q);
-                if (cand.empty()) break;
-                auto life = [&](int32_t q) { return (mate[q] >= 0 ? std::max(xend[q], xend[mate[q]]) : xend[q]) - phase_of[q]; };
-                std::sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b2) { return life(a) > life(b2); });
-                const size_t k = std::max<size_t>(1, static_cast<size_t>(cand.size() * std::min(0.5, 0.02 + double(n_smem - cap) / double(n_smem))));
-                for (size_t i = 0; i < k && i < cand.size(); ++i) {
-                    const int32_t q = cand[i];
-                    to_global[q] = 1;
-                    if (mate[q] >= 0) {
-                        to_global[mate[q]] = 1;
-                        second[mate[q]] = 0;
-                        mate[mate[q]] = -1;
-                        mate[q] = -1;
-                    }
-                }
-                allocate();
-            }
-            {
-                // per-warp register live set: values defined by or loaded into warp w, live from
-                // definition/first load to their last use in w (stores count as uses)
-                int64_t worst = 0, sum_peak = 0;
-                for (int w = 0; w < W; ++w) {
-                    std::vector<int64_t> first(N, -1), lastu(N, -1);
-                    int64_t pos = 0;
-                    for (int ph = 0; ph < P; ++ph)
-                        for (int32_t q : ts.seq[w][ph]) {
-                            const Node& nd = p.nodes[q];
-                            for (int k = 0; k < kArity[nd.op]; ++k) {
-                                const int32_t u = nd.arg[k];
-                                if (p.nodes[u].op == OP_CONST) continue;
-                                if (first[u] < 0) first[u] = pos;
-                                lastu[u] = pos;
-                            }
-                            first[q] = pos;
-                            if (lastu[q] < pos) lastu[q] = pos;
-                            if (xend[q] >= 0 || slot_of[q] >= 0 || !stores_of[q].empty()) lastu[q] = std::max(lastu[q], pos + 1);
-                            ++pos;
-                        }
-                    std::vector<int64_t> delta(pos + 2, 0);
-                    for (int64_t q = 0; q < N; ++q)
-                        if (first[q] >= 0) { delta[first[q]] += 1; delta[lastu[q] + 1] -= 1; }
-                    int64_t run = 0, peak = 0;
-                    for (int64_t i = 0; i <= pos; ++i) { run += delta[i]; peak = std::max(peak, run); }
-                    worst = std::max(worst, peak);
-                    sum_peak += peak;
-                }
-                if (getenv("VSB_LIVE_STATS"))
-                    fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
-                            double(sum_peak) / W);
-                ks.live_total = std::max(ks.live_total, sum_peak);  // ~ doubles per instance held in registers
-            }
-            ch.smem_slots = n_smem;
-            ch.overflow_slots = n_glob;
-            max_overflow = std::max(max_overflow, n_glob);
-            ch.smem_bytes = n_smem * IPB * rsz;
-
-            if (K > 1)
-                b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", K, nbuf);
-            else
-                b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
-            b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
-            b.put("    const int lane = threadIdx.x & 31;\n");
-            b.put("    const int wid = threadIdx.x >> 5;\n");
-            b.put("    const int grp = wid / %d;\n", Wl);
-            if (K > 1) {
-                b.put("    const int crank = (int)(blockIdx.x %% %d);\n", K);
-                b.put("    const long long cid = (long long)(blockIdx.x / %d);\n", K);
-            } else {
-                b.put("    const int crank = 0;\n");
-                b.put("    const long long cid = (long long)blockIdx.x;\n");
-            }
-            b.put("    const int warp = crank * %d + wid %% %d;\n", Wl, Wl);
-            // A.ipc <= VS_IPB instances per cluster (the runtime shrinks it so that the
-            // grid fills whole waves of SMs; the spare lanes idle)
-            // spare lanes mirror the last instance (identical bits; benign duplicate stores)
-            b.put("    long long t = cid * A.ipc + grp * 32 + lane;\n");
-            b.put("    if (grp * 32 + lane >= A.ipc || t >= A.n) t = A.n - 1;\n");
-            b.put("    const long long e = A.e0 + t;\n");
-            b.put("    (void)e;\n");
-            io_bases(b);
-            b.put("    real* __restrict__ S = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32 + lane;\n");
-            b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");
-            b.put("    real* __restrict__ X2 = vs_smem + (grp * 32 + lane) * 2;   // paired rows [row][lane][2]\n");
-            b.put("    (void)S; (void)X; (void)X2;\n");
-            if (K > 1) {
-                // shared::cluster addresses of this lane's X column in every CTA of the cluster
-                b.put("    const unsigned xl = (unsigned)__cvta_generic_to_shared(X);\n");
-                for (int r = 0; r < K; ++r)
-                    b.put("    unsigned XR%d; asm(\"mapa.shared::cluster.u32 %%0, %%1, %d;\" : \"=r\"(XR%d) : \"r\"(xl)); (void)XR%d;\n",
-                          r, r, r, r);
-                // every CTA of the cluster must be running before the first DSMEM store
-                b.put("    VS_CBAR();\n");
-            }
-            b.put("    switch (warp) {\n");
-            std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
-            for (int w = 0; w < W; ++w) {
-                b.put("    case %d: {\n", w);
-                const char* ind = "        ";
-                auto ensure = [&](int32_t u) {
-                    const Node& nu = p.nodes[u];
-                    if (nu.op == OP_CONST || have[u] == w) return;
-                    have[u] = w;
-                    if (nu.op == OP_INPUT) { input_load(b, u, ind); return; }
-                    if (!in_chunk(u)) {  // imported from an earlier chunk
-                        b.put("%sconst real v%d = S[%d * VS_IPB];\n", ind, u, slot_of[u]);
-                        ++ch.loads;
-                        return;
-                    }
-                    // produced by another warp in an earlier phase
-                    if (to_global[u]) {
-                        b.put("%sconst real v%d = S[%" PRId64 " * VS_IPB];\n", ind, u, cross_slots + xslot[u]);
-                    } else if (mate[u] >= 0) {
-                        const int32_t a0 = second[u] ? mate[u] : u, a1 = second[u] ? u : mate[u];
-                        b.put("%sconst vec2_t p%d = *reinterpret_cast<const vec2_t*>(X2 + %d * VS_IPB);\n", ind, a0, xslot[u]);
-                        b.put("%sconst real v%d = p%d.x, v%d = p%d.y;\n", ind, a0, a0, a1, a0);
-                        have[mate[u]] = w;
-                    } else {
-                        b.put("%sconst real v%d = X[%d * VS_IPB];\n", ind, u, xslot[u]);
-                    }
-                };
-                for (int32_t s : extra_stores[w]) {
-                    const int32_t u = p.stores[s].node;
-                    ensure(u);
-                    emit_store(b, s, opnd(u), ind, false);
-                }
-                for (int ph = 0; ph < P; ++ph) {
-                    for (int32_t q : ts.seq[w][ph]) {
-                        const Node& nd = p.nodes[q];
-                        if (sync_at[q] >= 0) b.put("%sVS_BSYNC(%d);\n", ind, 1 + sync_at[q] % 15);
-                        for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
-                        if (partner[q] >= 0 && warp_of[partner[q]] != w) {
-                            // mate lives on another warp: no pairing
-                            b.put("%sconst real v%d = %s;\n", ind, q, expr_of(nd).c_str());
-                            done[q] = 1;
-                        } else {
-                            emit_def(b, q, done, ind);
-                        }
-                        have[q] = w;
-                        if (xend[q] >= 0) {
-                            if (to_global[q]) {
-                                b.put("%sS[%" PRId64 " * VS_IPB] = v%d;\n", ind, cross_slots + xslot[q], q);
-                            } else {
-                                const int my = w / Wl;
-                                if (mate[q] >= 0) {
-                                    if (second[q])  // both defined now: one 128-bit store
-                                        b.put("%s*reinterpret_cast<vec2_t*>(X2 + %d * VS_IPB) = vec2_t{v%d, v%d};\n", ind,
-                                              xslot[q], mate[q], q);
-                                } else if (xranks[q] & (1u << my)) {
-                                    b.put("%sX[%d * VS_IPB] = v%d;\n", ind, xslot[q], q);
-                                }
-                                for (int r = 0; r < K; ++r) {
-                                    if (r == my || !(xranks[q] & (1u << r))) continue;
-                                    b.put("%sasm volatile(\"st.shared::cluster.%s [%%0+%" PRId64 "], %%1;\" :: \"r\"(XR%d), \"%s\"(v%d));\n",
-                                          ind, f32 ? "f32" : "f64", static_cast<int64_t>(xslot[q]) * IPB * rsz, r, f32 ? "f" : "d", q);
-                                    ++ch.remote_stores;
-                                }
-                            }
-                        }
-                        if (slot_of[q] >= 0) { b.put("%sS[%d * VS_IPB] = v%d;\n", ind, slot_of[q], q); ++ch.stores; }
-                        if (last)
-                            for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
-                    }
-                    if (split) {
-                        if (end_act[w][ph]) b.put(end_act[w][ph] == 2 ? "%sVS_BSYNC(%d);\n" : "%sVS_BARV(%d);\n", ind,
-                                                  1 + (ph - 1) % 15);
-                    } else if (ph + 1 < P) {
-                        b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
-                    }
-                }
-                b.put("        break;\n    }\n");
-            }
-            b.put("    }\n}\n");
-        }
+        if (team) emit_team_chunk(c, ch, b);
+        else emit_thread_chunk(c, ch, b);
         ch.source = hdr.s + b.s;
         ks.chunks.push_back(std::move(ch));
     }
@@ -1371,5 +1548,9 @@ Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag)
     }
     return ks;
 }
+
+}  // namespace
+
+Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) { return Emitter(p, opt, tag).run(); }
 
 }  // namespace vsb
