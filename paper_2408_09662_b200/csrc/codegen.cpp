@@ -1388,9 +1388,10 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     ch.smem_bytes = n_smem * IPB * rsz;
 
     if (K > 1)
-        b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", K, nbuf);
+        b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", K,
+              opt.min_blocks, nbuf);
     else
-        b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, 1) %s(const VsArgs A) {\n", nbuf);
+        b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
     b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
     b.put("    const int lane = threadIdx.x & 31;\n");
     b.put("    const int wid = threadIdx.x >> 5;\n");
