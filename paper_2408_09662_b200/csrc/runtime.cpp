@@ -603,7 +603,11 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
         dry.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
         dry.team_smem = p->opts.team_smem;
         dry.phase_cost = p->opts.phase_cost;
-        if (vsb::emit(p->prog, dry, "dry").live_total > 1500) p->opts.team = 8;
+        // and mid-width ones with 12 (ldlt_57, live sum 1456: team 12 / 16 = 0.377 / 0.427 ms at
+        // B=4096; srbm_mpc 1104 keeps 16: 0.410 / 0.433; profiles/r1_sweeps_r50_team_width.jsonl)
+        const int64_t live16 = vsb::emit(p->prog, dry, "dry").live_total;
+        if (live16 > 1500) p->opts.team = 8;
+        else if (live16 > 1200) p->opts.team = 12;
     }
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
