@@ -126,3 +126,12 @@ def test_thread_count_env_override(monkeypatch):
             default_thread_count()
     monkeypatch.delenv("VECSYM_THREADS")
     assert default_thread_count() == (os.cpu_count() or 1)
+
+
+def test_auto_team_width_follows_the_scheduled_live_set():
+    # >= 40k-op tapes: 16 warps unless the register live set at 16 warps is past the
+    # register file (measured in profiles/r1_sweeps_r50_team_width.jsonl)
+    want = {"srbm_mpc": 16, "ldlt_57": 12, "rbd_chain12": 8, "humanoid_rbd": 12, "pendulum": 0}
+    for name, team in want.items():
+        p = Plan(workloads.load_tape(name), cache_dir="", compile_threads=-1)
+        assert p.info["team"] == team, name
