@@ -363,3 +363,29 @@ def test_host_subranges_match_full(name):
         plan.eval_host(ws._in_buf.ctypes.data, ws._in_off, ws._out_buf.ctypes.data, ws._out_off, e0, e1, 0)
     for j in range(tape.n_out):
         assert_bitwise_or_nan(ws.output_matrix(j), full[j], f"{name} out {j}")
+
+
+@pytest.mark.parametrize("name", ["humanoid_rbd", "srbm_mpc"])
+def test_team_kernels_soa_layout_equals_aos(name):
+    # team kernels with [nnz, batch] (SoA) I/O (io_ld strides) == the AoS workspace layout, bitwise
+    from paper_2408_09662_b200 import Function
+
+    tape = workloads.load_tape(name)
+    B = 333
+    ins = workloads.make_inputs(name, B, seed=41)
+    aos = Function(tape)(*[torch.tensor(v, device="cuda") for v in ins])
+    soa = Function(tape, layout="soa")(*[torch.tensor(v.T.copy(), device="cuda") for v in ins])
+    for a, s in zip(aos, soa):
+        assert_bitwise_or_nan(a.cpu().numpy(), s.cpu().numpy().T, f"{name} soa")
+
+
+def test_team_kernels_fp32_mode_within_stated_tolerance():
+    # fp32 team kernels (humanoid_rbd, team 12): within the stated 1e-4 * max(|ref|, 1)
+    from paper_2408_09662_b200 import Function
+
+    tape = workloads.load_tape("humanoid_rbd")
+    ins = workloads.make_inputs("humanoid_rbd", 1024, seed=42)
+    ref = oracle.batch_eval(tape, ins)
+    outs = Function(tape, dtype=torch.float32)(*[torch.tensor(v, dtype=torch.float32, device="cuda") for v in ins])
+    for o, r in zip(outs, ref):
+        assert_close(o.double().cpu().numpy(), r, RTOL32, "fp32 team")
