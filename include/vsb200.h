@@ -13,6 +13,8 @@
  * and outputs mirror it with out_off / nnz_out.  The reference's `work`
  * argument has no counterpart: the work vector lives in registers.
  * The caller owns every buffer; plans own compiled code and device caches.
+ * Input and output buffers must not overlap (spare threads of the last block
+ * recompute the last instance and store its outputs again, bit-identical).
  *
  * All functions return VSB_OK (0) or an error code; vsb_last_error()
  * returns the calling thread's last message.  Plans are thread-safe;
@@ -27,7 +29,7 @@
 extern "C" {
 #endif
 
-#define VSB_ABI_VERSION 1
+#define VSB_ABI_VERSION 2   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions */
 
 enum vsb_status {
     VSB_OK = 0,
