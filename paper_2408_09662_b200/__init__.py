@@ -8,6 +8,7 @@ executed by generated sm_100a kernels (NVRTC) behind the C ABI in
 """
 
 from .batchrt import BatchWorkspace, batch_eval, default_thread_count, serial_eval
+from .hoist import InvariantSplit, split_invariant
 from .plan import Plan, clear_plan_cache, get_plan
 from .tape import (
     FORMAT_VERSION,
@@ -26,7 +27,7 @@ __all__ = [
     "BatchWorkspace", "batch_eval", "serial_eval", "default_thread_count",
     "Plan", "get_plan", "clear_plan_cache",
     "InstructionTape", "OpCode", "Sparsity", "arity", "as_tape", "deserialize", "serialize", "load", "save",
-    "FORMAT_VERSION", "Function",
+    "FORMAT_VERSION", "Function", "split_invariant", "InvariantSplit",
 ]
 
 __version__ = "0.1.0"

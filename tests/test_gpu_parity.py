@@ -279,6 +279,26 @@ def test_device_rollout_matches_host_loop(name, steps):
         state = res[0]
 
 
+@pytest.mark.parametrize("name", ["quad_step", "cartpole_rk4", "unicycle_mpc"])
+def test_hoisted_rollout_equals_unhoisted(name):
+    # loop-invariant rows evaluated once (hoist.split_invariant) == every step, bit for bit
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape(name)
+    B, steps = 300, 8
+    ins = workloads.make_inputs(name, B, seed=23)
+    res = []
+    for hoist in (True, False):
+        r = Rollout(tape, B, steps, hoist=hoist)
+        assert (r.split is not None) == hoist
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
+        traj, outs = r.run()
+        res.append((traj.cpu().numpy(), {j: o.cpu().numpy() for j, o in outs.items()}))
+    assert_bitwise_or_nan(res[0][0], res[1][0], f"{name} traj")
+    for j in res[1][1]:
+        assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"{name} out {j}")
+
+
 @pytest.mark.parametrize("name", ["pendulum", "cartpole_rk4", "example"])
 @pytest.mark.parametrize("B", [1, 127, 128, 129, 1000, 4103, 65536])
 def test_tma_tile_pipeline_equals_classic_kernel(name, B):
