@@ -29,14 +29,16 @@
 extern "C" {
 #endif
 
-#define VSB_ABI_VERSION 2   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions */
+#define VSB_ABI_VERSION 3   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
+                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED */
 
 enum vsb_status {
     VSB_OK = 0,
     VSB_ERR_INVALID = 1,   /* bad tape or arguments (Python: ValueError)        */
     VSB_ERR_COMPILE = 2,   /* NVRTC/ptxas failure (message carries the log)     */
     VSB_ERR_CUDA = 3,      /* CUDA runtime error (no device, launch failure...) */
-    VSB_ERR_NOMEM = 4
+    VSB_ERR_NOMEM = 4,
+    VSB_ERR_UNSUPPORTED = 5 /* the plan has no variant for this call (caller falls back) */
 };
 
 enum vsb_dtype { VSB_F64 = 0, VSB_F32 = 1 };
@@ -140,6 +142,20 @@ int vsb_eval_device_ptrs(vsb_plan *plan, const void *const *ins, void *const *ou
  * `ins`/`outs` are HOST arrays of device pointers.  Coalesced without staging. */
 int vsb_eval_device_soa(vsb_plan *plan, const void *const *ins, void *const *outs, int64_t ld,
                         int64_t e0, int64_t e1, int32_t device, void *stream);
+
+/* Closed-loop rollout on the device, one launch: `steps` evaluations of
+ * state_{k+1} = f(state_k, other inputs), the state (input `state_in`, fed by
+ * output `state_out`, same nonzero count) kept in registers between steps.
+ * Time-major AoS planes of `plane` instances: ins[state_in] is the initial
+ * state plane; output j of step k is written at outs[j] + (k * plane + e) *
+ * nnz_out[j] + nz (so outs[state_out] is usually trajectory plane 1); the
+ * other inputs are read every step.  Bitwise equal to `steps` chained
+ * vsb_eval_device calls.  VSB_ERR_UNSUPPORTED when the plan is not a single
+ * thread-per-instance kernel or a state nonzero is never stored.
+ * Replaces: quadsim.rollout_batch's host loop (quadsim.py:298-303). */
+int vsb_rollout_device(vsb_plan *plan, int32_t state_in, int32_t state_out, const void *const *ins,
+                       void *const *outs, int64_t plane, int64_t steps, int64_t e0, int64_t e1,
+                       int32_t device, void *stream);
 
 /* End-to-end over HOST memory (pinned or pageable), synchronous: H2D of the
  * inputs, the kernel chain, D2H of the outputs, pipelined in pieces over

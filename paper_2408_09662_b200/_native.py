@@ -14,17 +14,21 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvsb200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
-VSB_OK, VSB_ERR_INVALID, VSB_ERR_COMPILE, VSB_ERR_CUDA, VSB_ERR_NOMEM = range(5)
+VSB_OK, VSB_ERR_INVALID, VSB_ERR_COMPILE, VSB_ERR_CUDA, VSB_ERR_NOMEM, VSB_ERR_UNSUPPORTED = range(6)
 VSB_F64, VSB_F32 = 0, 1
 
 # every symbol include/vsb200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "vsb_version", "vsb_last_error", "vsb_options_init", "vsb_plan_create", "vsb_plan_destroy",
     "vsb_plan_get_info", "vsb_plan_source", "vsb_plan_cubin", "vsb_plan_log", "vsb_eval_device", "vsb_eval_device_ptrs",
-    "vsb_eval_device_soa",
+    "vsb_eval_device_soa", "vsb_rollout_device",
     "vsb_eval_host", "vsb_eval_host_sharded", "vsb_transpose", "vsb_launches_per_eval",
     "vsb_host_alloc", "vsb_host_free",
 )
+
+
+class UnsupportedError(RuntimeError):
+    """The plan has no variant for the requested call (VSB_ERR_UNSUPPORTED); callers fall back."""
 
 
 class NativeLibraryError(RuntimeError):
@@ -134,6 +138,7 @@ def lib() -> ctypes.CDLL:
     L.vsb_eval_device.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32, vp]
     L.vsb_eval_device_ptrs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i32, vp]
     L.vsb_eval_device_soa.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i32, vp]
+    L.vsb_rollout_device.argtypes = [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i64, i32, vp]
     L.vsb_eval_host.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32]
     L.vsb_eval_host_sharded.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, ctypes.POINTER(i32), i32]
     L.vsb_transpose.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
@@ -162,4 +167,6 @@ def check(rc: int) -> None:
         raise CudaError(msg)
     if rc == VSB_ERR_NOMEM:
         raise MemoryError(msg)
+    if rc == VSB_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
     raise RuntimeError(f"vsb error {rc}: {msg}")

@@ -517,7 +517,9 @@ private:
     void emit_store(Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) const;
     void input_load(Out& o, int32_t u, const char* ind) const;
     void io_bases(Out& o) const;
-    void emit_direct_body(Out& b, const Chunk& ch, bool ldg) const;
+    void emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll = false) const;
+    bool roll_possible() const;
+    void emit_roll_kernel(Chunk& ch, Out& b) const;
     void emit_thread_chunk(int c, Chunk& ch, Out& b);
     void emit_tma_kernel(Chunk& ch, Out& b) const;
     void emit_team_chunk(int c, Chunk& ch, Out& b);
@@ -810,32 +812,76 @@ void Emitter::io_bases(Out& o) const {
         for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
 }
 
-void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg) const {
+void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll) const {
     // ops of the chunk with direct I/O: inputs `I<i>[k]` (smem tile row) or `__ldg(I<i> + k)`
-    // (global row), outputs `O<j>[k] = v`; one thread per instance, no scratch
+    // (global row), outputs `O<j>[k] = v`; one thread per instance, no scratch.  `roll`: the
+    // state input `opt.roll_in` reads registers `st<k>`, stores to `opt.roll_out` also set `nt<k>`
     const char* ind = "        ";
     std::vector<uint8_t> dn(N, 0), got(N, 0);
     auto ensure = [&](int32_t u) {
         const Node& nu = p.nodes[u];
         if (nu.op != OP_INPUT || got[u]) return;
         got[u] = 1;
-        if (ldg) b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
+        if (roll && nu.in_i == opt.roll_in) b.put("%sconst real v%d = st%d;\n", ind, u, nu.in_k);
+        else if (ldg) b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
         else b.put("%sconst real v%d = I%d[%d];\n", ind, u, nu.in_i, nu.in_k);
+    };
+    auto store = [&](size_t si, const std::string& val) {
+        const Store& st = p.stores[si];
+        b.put("%sO%d[%d] = %s;\n", ind, st.j, st.k, val.c_str());
+        if (roll && st.j == opt.roll_out) b.put("%snt%d = %s;\n", ind, st.k, val.c_str());
     };
     for (size_t si = 0; si < p.stores.size(); ++si) {
         const int32_t u = p.stores[si].node;
         if (p.nodes[u].op > OP_INPUT) continue;
         ensure(u);
-        b.put("%sO%d[%d] = %s;\n", ind, p.stores[si].j, p.stores[si].k, opnd(u).c_str());
+        store(si, opnd(u));
     }
     for (int64_t q = ch.first; q < ch.last; ++q) {
         const Node& nd = p.nodes[q];
         if (nd.op <= OP_ASSIGN) continue;
         for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
         emit_def(b, q, dn, ind);
-        for (int32_t si : stores_of[q])
-            b.put("%sO%d[%d] = v%" PRId64 ";\n", ind, p.stores[si].j, p.stores[si].k, q);
+        for (int32_t si : stores_of[q]) store(static_cast<size_t>(si), "v" + std::to_string(q));
     }
+}
+
+// a closed-loop kernel needs one kernel, AoS I/O, matching state sizes and every nonzero of
+// the state output stored (an unstored one would carry the buffer's old contents)
+bool Emitter::roll_possible() const {
+    if (opt.roll_in < 0 || opt.roll_out < 0 || opt.roll_in >= n_in || opt.roll_out >= n_out) return false;
+    if (!same_kernel || soa || team) return false;
+    const int64_t n = p.nnz_in[opt.roll_in];
+    if (n == 0 || n != p.nnz_out[opt.roll_out]) return false;
+    std::vector<uint8_t> seen(static_cast<size_t>(n), 0);
+    for (const Store& st : p.stores)
+        if (st.j == opt.roll_out) seen[st.k] = 1;
+    for (uint8_t x : seen)
+        if (!x) return false;
+    return true;
+}
+
+// K steps of state_{k+1} = f(state_k, params) in one launch: the state
+// stays in registers between steps; every step's outputs are stored time-major
+// (out[j] + k * A.ipc * nnz_out[j]; A.ipc = instances per time plane, A.ld = steps)
+void Emitter::emit_roll_kernel(Chunk& ch, Out& b) const {
+    ch.roll = true;
+    const int64_t n = p.nnz_in[opt.roll_in];
+    b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_roll(const VsArgs A) {\n", opt.min_blocks, ch.name.c_str());
+    b.put("    long long t = (long long)blockIdx.x * VS_BS + threadIdx.x;\n");
+    b.put("    if (t >= A.n) t = A.n - 1;\n");
+    b.put("    const long long e = A.e0 + t;\n");
+    for (int i = 0; i < n_in; ++i)
+        b.put("    const real* __restrict__ I%d = A.in[%d] + e * %" PRId64 "LL;\n    (void)I%d;\n", i, i, p.nnz_in[i], i);
+    for (int j = 0; j < n_out; ++j)
+        b.put("    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
+    for (int64_t k = 0; k < n; ++k) b.put("    real st%" PRId64 " = __ldg(I%d + %" PRId64 ");\n", k, opt.roll_in, k);
+    b.put("    for (long long step = 0; step < A.ld; ++step) {\n");
+    for (int64_t k = 0; k < n; ++k) b.put("        real nt%" PRId64 ";\n", k);
+    emit_direct_body(b, ch, true, true);
+    for (int64_t k = 0; k < n; ++k) b.put("        st%" PRId64 " = nt%" PRId64 ";\n", k, k);
+    for (int j = 0; j < n_out; ++j) b.put("        O%d += A.ipc * %" PRId64 "LL;\n", j, p.nnz_out[j]);
+    b.put("    }\n}\n");
 }
 
 // ================= one thread per instance =================
@@ -927,6 +973,7 @@ void Emitter::emit_thread_chunk(int c, Chunk& ch, Out& b) {
     const bool tma = opt.bulk_io && same_kernel && !soa && ni_tot > 0 && no_tot > 0 &&
                      2 * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
     if (tma) emit_tma_kernel(ch, b);
+    if (roll_possible()) emit_roll_kernel(ch, b);
 }
 
 void Emitter::emit_tma_kernel(Chunk& ch, Out& b) const {

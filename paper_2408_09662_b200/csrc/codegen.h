@@ -91,6 +91,9 @@ struct EmitOptions {
     bool pair_xfers = false;   // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
     bool split_barriers = false;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
     bool bulk_io = true;       // thread mode, single kernel: also emit a persistent TMA (cp.async.bulk) variant
+    // thread mode, single kernel: also emit `<name>_roll`, a K-step closed-loop kernel feeding
+    // output `roll_out` back into input `roll_in` in registers (-1: none)
+    int roll_in = -1, roll_out = -1;
 };
 
 struct Chunk {
@@ -103,6 +106,7 @@ struct Chunk {
     int inst_per_block = 128;      // instances per CTA (cluster in team mode: 32 * groups)
     int cluster = 1;               // CTAs per cluster (grid = clusters * cluster)
     bool tma = false;              // the source also holds `<name>_tma` (persistent bulk-copy variant)
+    bool roll = false;             // the source also holds `<name>_roll` (multi-step rollout kernel)
     int64_t tma_smem_bytes = 0;
     // team-mode schedule statistics
     int64_t phases = 0, smem_slots = 0, overflow_slots = 0, xfers = 0, remote_stores = 0, pairs = 0;

@@ -212,6 +212,7 @@ struct Variant {
     std::vector<cudaLibrary_t> libs;     // loaded lazily (context-independent)
     std::vector<cudaKernel_t> kerns;
     cudaKernel_t tma_kern = nullptr;                // persistent bulk-copy variant of chunk 0 (if emitted)
+    cudaKernel_t roll_kern = nullptr;               // multi-step rollout variant of chunk 0 (roll layouts)
     std::map<int, int> tma_grid;                    // device -> resident CTAs (occupancy x SMs)
     std::set<int> attr_devices;          // devices on which smem attributes are set
     double compile_seconds = 0.0;
@@ -246,6 +247,8 @@ struct vsb_plan {
 
 namespace {
 
+constexpr int kRollKey = 1 << 20;
+
 int build_variant(vsb_plan* p, int layout, Variant** out) {
     auto it = p->variants.find(layout);
     if (it != p->variants.end()) {
@@ -256,6 +259,12 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     vsb::EmitOptions eo;
     eo.f32 = p->opts.dtype == VSB_F32;
     eo.layout = layout == VSB_SOA ? vsb::Layout::SOA : vsb::Layout::AOS;
+    // rollout variants (vsb_rollout_device): key kRollKey + state_in * 65536 + state_out
+    const bool roll = layout >= kRollKey;
+    if (roll) {
+        eo.roll_in = (layout - kRollKey) / 65536;
+        eo.roll_out = (layout - kRollKey) % 65536;
+    }
     eo.block = p->opts.block;
     eo.min_blocks = p->opts.min_blocks;
     eo.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
@@ -271,13 +280,14 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.team_smem = p->opts.team_smem;
     eo.groups = p->opts.groups;
     eo.cluster = p->opts.cluster;
-    eo.bulk_io = p->opts.bulk_io >= 0;
+    eo.bulk_io = p->opts.bulk_io >= 0 && !roll;
     eo.outline = p->opts.outline < 0 ? 0 : (p->opts.outline == 0 ? (eo.team >= 2 ? 3 : 0) : p->opts.outline);
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
     if (eo.outline) shape += "o" + std::to_string(eo.outline);
     if (!eo.bulk_io) shape += "nb";
+    if (roll) shape += "r" + std::to_string(eo.roll_in) + "_" + std::to_string(eo.roll_out);
     v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
 
     std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
@@ -336,6 +346,8 @@ int ensure_loaded(Variant* v, int device) {
         }
         if (C == 1 && v->ks.chunks[0].tma)
             CUDA_TRY(cudaLibraryGetKernel(&v->tma_kern, v->libs[0], (v->ks.chunks[0].name + "_tma").c_str()));
+        if (C == 1 && v->ks.chunks[0].roll)
+            CUDA_TRY(cudaLibraryGetKernel(&v->roll_kern, v->libs[0], (v->ks.chunks[0].name + "_roll").c_str()));
     }
     if (!v->attr_devices.count(device)) {
         for (size_t c = 0; c < v->kerns.size(); ++c) {
@@ -760,6 +772,48 @@ int vsb_eval_device_ptrs(vsb_plan* p, const void* const* ins_, void* const* outs
     std::vector<const void*> ins(ins_, ins_ + n_in);
     std::vector<void*> outs(outs_, outs_ + n_out);
     return launch_chain(p, v, ins, outs, e0, e1 - e0, 0, static_cast<cudaStream_t>(stream), device);
+}
+
+int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const void* const* ins_,
+                       void* const* outs_, int64_t plane, int64_t steps, int64_t e0, int64_t e1, int32_t device,
+                       void* stream) {
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if (state_in < 0 || state_in >= n_in || state_out < 0 || state_out >= n_out)
+        return fail(VSB_ERR_INVALID, "state input/output index out of range");
+    if (p->prog.nnz_in[state_in] != p->prog.nnz_out[state_out])
+        return fail(VSB_ERR_INVALID, "state input and output sizes differ");
+    if (steps < 0 || plane < e1) return fail(VSB_ERR_INVALID, "need steps >= 0 and plane >= e1");
+    if (e1 == e0 || steps == 0) return VSB_OK;
+    if (!ins_ || !outs_) return fail(VSB_ERR_INVALID, "null pointer array");
+    CUDA_TRY(cudaSetDevice(device));
+    Variant* v;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = build_variant(p, kRollKey + state_in * 65536 + state_out, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+    }
+    if (rc != VSB_OK) return rc;
+    if (!v->roll_kern)
+        return fail(VSB_ERR_UNSUPPORTED, "no single-kernel closed-loop variant for this tape (multi-kernel or "
+                                         "team plan, or a state nonzero the tape never stores)");
+    const auto& ch = v->ks.chunks[0];
+    const int64_t n = e1 - e0, BSz = ch.threads;
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
+    for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins_[i]);
+    for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs_[j]);
+    const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
+    pb[base + 1] = static_cast<uint64_t>(e0);
+    pb[base + 2] = static_cast<uint64_t>(n);
+    pb[base + 3] = static_cast<uint64_t>(steps);
+    pb[base + 5] = static_cast<uint64_t>(plane);
+    void* args[] = {pb.data()};
+    cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->roll_kern),
+                                     dim3(static_cast<unsigned>((n + BSz - 1) / BSz)), dim3(ch.threads), args, 0,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + ch.name + "_roll): " + cudaGetErrorString(e));
+    return VSB_OK;
 }
 
 int vsb_eval_device_soa(vsb_plan* p, const void* const* ins_, void* const* outs_, int64_t ld, int64_t e0, int64_t e1,

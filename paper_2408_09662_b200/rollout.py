@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import torch
 
+from ._native import UnsupportedError
 from .hoist import split_invariant
 from .plan import get_plan
 from .tape import as_tape
@@ -31,11 +32,14 @@ class Rollout:
     ``traj [steps+1, B, n]`` and per-step outputs; ``set(state0, params)`` loads
     inputs (device tensors, copied in); ``run()`` replays the graph.
     ``hoist``: True / False / None (auto: when at least as many arithmetic rows
-    are state-independent as not, and at least 64).
+    are state-independent as not, and at least 64).  ``fused``: run the K steps
+    as ONE kernel with the state in registers (``vsb_rollout_device``) when the
+    step is a single thread-per-instance kernel; None = whenever possible.
     """
 
     def __init__(self, tape, batch: int, steps: int, *, state_in: int = 0, state_out: int = 0,
-                 device=None, use_graph: bool = True, hoist=None, **plan_options):
+                 device=None, use_graph: bool = True, hoist=None, fused=None,
+                 **plan_options):
         tape = as_tape(tape)
         if steps < 1:
             raise ValueError(f"steps must be >= 1, got {steps}")
@@ -65,6 +69,7 @@ class Rollout:
         self.others = [j for j in range(tape.n_out) if j != state_out]
         self.outs = {j: torch.empty((steps, B, tape.nnz_out[j]), dtype=torch.float64, device=dev)
                      for j in self.others}
+        self.fused = fused is not False
         self.boundary = (torch.empty((B, self.split.boundary), dtype=torch.float64, device=dev)
                          if self.split is not None else None)
         self.graph = None
@@ -84,6 +89,19 @@ class Rollout:
         if self.split is not None:
             self.pre_plan.eval_device_ptrs([self.params[i].data_ptr() for i in self.split.fixed],
                                            [self.boundary.data_ptr()], 0, self.B, dev, s.cuda_stream)
+        if self.fused:
+            si = 0 if self.split is not None else self.state_in
+            ins = [self.traj[0].data_ptr() if i == si else
+                   (self.boundary.data_ptr() if self.split is not None else self.params[i].data_ptr())
+                   for i in range(self.plan.tape.n_in)]
+            outs = [self.traj[1].data_ptr() if j == self.state_out else self.outs[j][0].data_ptr()
+                    for j in range(t.n_out)]
+            try:
+                self.plan.rollout_device(si, self.state_out, ins, outs, self.B, self.steps, 0, self.B, dev,
+                                         s.cuda_stream)
+                return
+            except UnsupportedError:
+                self.fused = False
         for k in range(self.steps):
             if self.split is not None:
                 ins = [self.traj[k].data_ptr(), self.boundary.data_ptr()]
@@ -97,7 +115,7 @@ class Rollout:
     @property
     def launches_per_run(self) -> int:
         pre = self.pre_plan.launches_per_eval(self.B) if self.pre_plan is not None else 0
-        return pre + self.steps * self.plan.launches_per_eval(self.B)
+        return pre + (1 if self.fused else self.steps * self.plan.launches_per_eval(self.B))
 
     def set(self, state0, params):
         params = list(params)

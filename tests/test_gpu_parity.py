@@ -299,6 +299,33 @@ def test_hoisted_rollout_equals_unhoisted(name):
         assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"{name} out {j}")
 
 
+@pytest.mark.parametrize("name, hoist, expect_fused", [("pendulum", False, True), ("cartpole_rk4", False, True),
+                                                       ("quad_step", True, True), ("quad_step", False, False)])
+@pytest.mark.parametrize("B", [1, 129, 3000])
+def test_fused_rollout_kernel_equals_step_loop(name, hoist, expect_fused, B):
+    # one closed-loop launch (state in registers, vsb_rollout_device) == K chained evaluations, bitwise
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape(name)
+    steps = 12
+    ins = workloads.make_inputs(name, B, seed=29)
+    res = []
+    for fused in (True, False):
+        r = Rollout(tape, B, steps, hoist=hoist, fused=fused, use_graph=False)
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
+        traj, outs = r.run()
+        if fused:
+            # team-mode (multi-warp) plans fall back to the step loop
+            assert r.fused == expect_fused
+            if expect_fused:
+                assert r.launches_per_run == 1 + (r.pre_plan.launches_per_eval(B) if hoist else 0)
+        res.append((traj.cpu().numpy(), {j: o.cpu().numpy() for j, o in outs.items()}, r.fused))
+    assert res[1][2] is False
+    assert_bitwise_or_nan(res[0][0], res[1][0], f"{name} traj")
+    for j in res[1][1]:
+        assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"{name} out {j}")
+
+
 @pytest.mark.parametrize("name", ["pendulum", "cartpole_rk4", "example"])
 @pytest.mark.parametrize("B", [1, 127, 128, 129, 1000, 4103, 65536])
 def test_tma_tile_pipeline_equals_classic_kernel(name, B):
