@@ -35,11 +35,15 @@ class Rollout:
     are state-independent as not, and at least 64).  ``fused``: run the K steps
     as ONE kernel with the state in registers (``vsb_rollout_device``) when the
     step is a single thread-per-instance kernel; None = whenever possible.
+    ``dedup``: with hoisting, evaluate the ``pre`` tape once per DISTINCT
+    parameter row (bit patterns; ``rollout_batch`` broadcasts one theta,
+    ``roa_scan`` has one per thrust limit) and gather; None = when at most half
+    the rows are distinct.
     """
 
     def __init__(self, tape, batch: int, steps: int, *, state_in: int = 0, state_out: int = 0,
                  device=None, use_graph: bool = True, hoist=None, fused=None,
-                 **plan_options):
+                 dedup=None, **plan_options):
         tape = as_tape(tape)
         if steps < 1:
             raise ValueError(f"steps must be >= 1, got {steps}")
@@ -72,21 +76,30 @@ class Rollout:
         self.fused = fused is not False
         self.boundary = (torch.empty((B, self.split.boundary), dtype=torch.float64, device=dev)
                          if self.split is not None else None)
+        self.use_graph, self.dedup = use_graph, dedup
+        self.u_count, self.u_params, self.u_boundary = 0, None, None
+        self.inv = torch.zeros(B, dtype=torch.int64, device=dev) if self.split is not None else None
         self.graph = None
-        if use_graph:
-            stream = torch.cuda.current_stream(dev)
-            side = torch.cuda.Stream(device=dev)
-            side.wait_stream(stream)
-            with torch.cuda.stream(side):
-                self._launch(side)  # warm-up: loads modules, primes the scratch pool
-            stream.wait_stream(side)
-            self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph):
-                self._launch(torch.cuda.current_stream(dev))
+
+    def _capture(self):
+        dev = self.dev
+        stream = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            self._launch(side)  # warm-up: loads modules, primes the scratch pool
+        stream.wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._launch(torch.cuda.current_stream(dev))
 
     def _launch(self, s):
         t, dev = self.tape, self.dev.index or 0
-        if self.split is not None:
+        if self.split is not None and self.u_count:
+            self.pre_plan.eval_device_ptrs([p.data_ptr() for p in self.u_params], [self.u_boundary.data_ptr()],
+                                           0, self.u_count, dev, s.cuda_stream)
+            torch.index_select(self.u_boundary, 0, self.inv, out=self.boundary)
+        elif self.split is not None:
             self.pre_plan.eval_device_ptrs([self.params[i].data_ptr() for i in self.split.fixed],
                                            [self.boundary.data_ptr()], 0, self.B, dev, s.cuda_stream)
         if self.fused:
@@ -127,8 +140,34 @@ class Rollout:
         for i, p in enumerate(params):
             if i != self.state_in:
                 self.params[i].copy_(torch.as_tensor(p, dtype=torch.float64))
+        if self.split is not None and self.split.fixed and self.dedup is not False:
+            self._dedup()
+
+    def _dedup(self):
+        fixed = self.split.fixed
+        rows = torch.cat([self.params[i] for i in fixed], 1).contiguous().view(torch.int64)
+        uniq, inv = torch.unique(rows, dim=0, return_inverse=True)   # by bit pattern: +-0 and NaNs kept apart
+        U = int(uniq.shape[0])
+        if self.dedup is None and 2 * U > self.B:
+            if self.u_count:
+                self.u_count, self.graph = 0, None
+            return
+        uniq = uniq.view(torch.float64)
+        if U != self.u_count:
+            self.u_count, self.graph = U, None
+            self.u_params = [torch.empty((U, self.tape.nnz_in[i]), dtype=torch.float64, device=self.dev)
+                             for i in fixed]
+            self.u_boundary = torch.empty((U, self.split.boundary), dtype=torch.float64, device=self.dev)
+        col = 0
+        for p, i in zip(self.u_params, fixed):
+            nz = self.tape.nnz_in[i]
+            p.copy_(uniq[:, col:col + nz])
+            col += nz
+        self.inv.copy_(inv.view(-1))
 
     def run(self):
+        if self.use_graph and self.graph is None:
+            self._capture()
         if self.graph is not None:
             self.graph.replay()
         else:

@@ -299,6 +299,37 @@ def test_hoisted_rollout_equals_unhoisted(name):
         assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"{name} out {j}")
 
 
+@pytest.mark.parametrize("distinct", [1, 3])
+def test_rollout_dedup_of_parameter_rows(distinct):
+    # rollout_batch broadcasts one theta, roa_scan has one per thrust limit: the hoisted
+    # pre tape runs once per distinct row (by bit pattern) and is gathered -- bitwise the same
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape("quad_step")
+    B, steps = 600, 10
+    ins = workloads.make_inputs("quad_step", B, seed=31)
+    theta = np.repeat(ins[1][:1], B, axis=0)
+    if distinct == 3:
+        # rows 3k / 3k+1 differ only in the sign of a zero: distinct by bit pattern
+        theta[0::3, 0] = 0.0
+        theta[1::3, 0] = -0.0
+        theta[2::3] = ins[1][1]
+    res = []
+    for dedup in (None, False):
+        r = Rollout(tape, B, steps, dedup=dedup)
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(theta, device="cuda")])
+        traj, outs = r.run()
+        if dedup is None:
+            assert r.u_count == distinct
+        res.append((traj.cpu().numpy(), {j: o.cpu().numpy() for j, o in outs.items()}))
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(theta, device="cuda")])  # re-set keeps the graph
+        traj2, _ = r.run()
+        assert_bitwise_or_nan(traj2.cpu().numpy(), res[-1][0], "re-run")
+    assert_bitwise_or_nan(res[0][0], res[1][0], "traj")
+    for j in res[1][1]:
+        assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"out {j}")
+
+
 @pytest.mark.parametrize("name, hoist, expect_fused", [("pendulum", False, True), ("cartpole_rk4", False, True),
                                                        ("quad_step", True, True), ("quad_step", False, False)])
 @pytest.mark.parametrize("B", [1, 129, 3000])

@@ -32,12 +32,17 @@ def main():
     ap.add_argument("--team", type=int, default=0)
     ap.add_argument("--hoist", choices=["auto", "on", "off"], default="auto")
     ap.add_argument("--fused", choices=["auto", "off"], default="auto")
+    ap.add_argument("--shared-theta", action="store_true", help="one parameter row for every env (rollout_batch's broadcast)")
+    ap.add_argument("--dedup", choices=["auto", "off"], default="auto")
     args = ap.parse_args()
     tape = workloads.load_tape(args.workload)
     ins = workloads.make_inputs(args.workload, args.batch, seed=5)
+    if args.shared_theta:
+        ins = [ins[0]] + [np.repeat(v[:1], args.batch, axis=0) for v in ins[1:]]
     opts = {"team": args.team} if args.team else {}
     hoist = {"auto": None, "on": True, "off": False}[args.hoist]
-    r = Rollout(tape, args.batch, args.steps, hoist=hoist, fused=None if args.fused == "auto" else False, **opts)
+    r = Rollout(tape, args.batch, args.steps, hoist=hoist, fused=None if args.fused == "auto" else False,
+                dedup=None if args.dedup == "auto" else False, **opts)
     r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
     r.run()
     torch.cuda.synchronize()
@@ -67,7 +72,8 @@ def main():
                       "gpu_env_steps_per_s": gpu_rate, "cpu_env_steps_per_s": cpu_rate, "cpu_threads": threads,
                       "cpu_sample": f"{Bs} envs x {k_cpu} steps", "speedup": gpu_rate / cpu_rate,
                       "launches_per_rollout": r.launches_per_run, "plan": r.plan.info["team"],
-                      "hoisted_rows": r.split.hoisted_rows if r.split is not None else 0, "fused": r.fused}),
+                      "hoisted_rows": r.split.hoisted_rows if r.split is not None else 0, "fused": r.fused,
+                      "distinct_param_rows": r.u_count or None, "shared_theta": args.shared_theta}),
           flush=True)
 
 
