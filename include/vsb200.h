@@ -149,13 +149,15 @@ int vsb_eval_device_soa(vsb_plan *plan, const void *const *ins, void *const *out
  * Time-major AoS planes of `plane` instances: ins[state_in] is the initial
  * state plane; output j of step k is written at outs[j] + (k * plane + e) *
  * nnz_out[j] + nz (so outs[state_out] is usually trajectory plane 1); the
- * other inputs are read every step.  Bitwise equal to `steps` chained
+ * other inputs are read every step.  `record` = 0: no per-step outputs, only
+ * the final state, to outs[state_out] (roa_scan's mode, quadsim.py:363-369).
+ * Bitwise equal to `steps` chained
  * vsb_eval_device calls.  VSB_ERR_UNSUPPORTED when the plan is not a single
  * thread-per-instance kernel or a state nonzero is never stored.
  * Replaces: quadsim.rollout_batch's host loop (quadsim.py:298-303). */
 int vsb_rollout_device(vsb_plan *plan, int32_t state_in, int32_t state_out, const void *const *ins,
-                       void *const *outs, int64_t plane, int64_t steps, int64_t e0, int64_t e1,
-                       int32_t device, void *stream);
+                       void *const *outs, int64_t plane, int64_t steps, int32_t record, int64_t e0,
+                       int64_t e1, int32_t device, void *stream);
 
 /* End-to-end over HOST memory (pinned or pageable), synchronous: H2D of the
  * inputs, the kernel chain, D2H of the outputs, pipelined in pieces over

@@ -138,7 +138,8 @@ def lib() -> ctypes.CDLL:
     L.vsb_eval_device.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32, vp]
     L.vsb_eval_device_ptrs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i32, vp]
     L.vsb_eval_device_soa.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i32, vp]
-    L.vsb_rollout_device.argtypes = [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i64, i32, vp]
+    L.vsb_rollout_device.argtypes = [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i32, i64, i64, i32,
+                                     vp]
     L.vsb_eval_host.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32]
     L.vsb_eval_host_sharded.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, ctypes.POINTER(i32), i32]
     L.vsb_transpose.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]

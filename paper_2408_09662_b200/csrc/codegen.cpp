@@ -828,7 +828,7 @@ void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll) con
     };
     auto store = [&](size_t si, const std::string& val) {
         const Store& st = p.stores[si];
-        b.put("%sO%d[%d] = %s;\n", ind, st.j, st.k, val.c_str());
+        b.put(roll ? "%sif (rec) O%d[%d] = %s;\n" : "%sO%d[%d] = %s;\n", ind, st.j, st.k, val.c_str());
         if (roll && st.j == opt.roll_out) b.put("%snt%d = %s;\n", ind, st.k, val.c_str());
     };
     for (size_t si = 0; si < p.stores.size(); ++si) {
@@ -862,8 +862,9 @@ bool Emitter::roll_possible() const {
 }
 
 // K steps of state_{k+1} = f(state_k, params) in one launch: the state
-// stays in registers between steps; every step's outputs are stored time-major
-// (out[j] + k * A.ipc * nnz_out[j]; A.ipc = instances per time plane, A.ld = steps)
+// stays in registers between steps; A.io_ld == 0: every step's outputs are stored time-major
+// (out[j] + k * A.ipc * nnz_out[j]; A.ipc = instances per time plane, A.ld = steps);
+// A.io_ld == 1: only the final state, to out[roll_out] (roa_scan's trajectory-free mode)
 void Emitter::emit_roll_kernel(Chunk& ch, Out& b) const {
     ch.roll = true;
     const int64_t n = p.nnz_in[opt.roll_in];
@@ -876,11 +877,15 @@ void Emitter::emit_roll_kernel(Chunk& ch, Out& b) const {
     for (int j = 0; j < n_out; ++j)
         b.put("    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
     for (int64_t k = 0; k < n; ++k) b.put("    real st%" PRId64 " = __ldg(I%d + %" PRId64 ");\n", k, opt.roll_in, k);
+    b.put("    const bool rec = A.io_ld == 0;\n");
     b.put("    for (long long step = 0; step < A.ld; ++step) {\n");
     for (int64_t k = 0; k < n; ++k) b.put("        real nt%" PRId64 ";\n", k);
     emit_direct_body(b, ch, true, true);
     for (int64_t k = 0; k < n; ++k) b.put("        st%" PRId64 " = nt%" PRId64 ";\n", k, k);
-    for (int j = 0; j < n_out; ++j) b.put("        O%d += A.ipc * %" PRId64 "LL;\n", j, p.nnz_out[j]);
+    b.put("        if (rec) {\n");
+    for (int j = 0; j < n_out; ++j) b.put("            O%d += A.ipc * %" PRId64 "LL;\n", j, p.nnz_out[j]);
+    b.put("        }\n    }\n    if (!rec) {\n");
+    for (int64_t k = 0; k < n; ++k) b.put("        O%d[%" PRId64 "] = st%" PRId64 ";\n", opt.roll_out, k, k);
     b.put("    }\n}\n");
 }
 

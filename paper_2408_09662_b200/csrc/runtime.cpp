@@ -775,8 +775,8 @@ int vsb_eval_device_ptrs(vsb_plan* p, const void* const* ins_, void* const* outs
 }
 
 int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const void* const* ins_,
-                       void* const* outs_, int64_t plane, int64_t steps, int64_t e0, int64_t e1, int32_t device,
-                       void* stream) {
+                       void* const* outs_, int64_t plane, int64_t steps, int32_t record, int64_t e0, int64_t e1,
+                       int32_t device, void* stream) {
     int rc = check_range(p, e0, e1);
     if (rc != VSB_OK) return rc;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
@@ -807,6 +807,7 @@ int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const v
     pb[base + 1] = static_cast<uint64_t>(e0);
     pb[base + 2] = static_cast<uint64_t>(n);
     pb[base + 3] = static_cast<uint64_t>(steps);
+    pb[base + 4] = record ? 0u : 1u;
     pb[base + 5] = static_cast<uint64_t>(plane);
     void* args[] = {pb.data()};
     cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->roll_kern),

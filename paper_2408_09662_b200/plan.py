@@ -140,13 +140,15 @@ class Plan:
         check(_native.lib().vsb_eval_device_soa(self._h, ins, outs, int(ld), int(e0), int(e1), int(device),
                                                 ctypes.c_void_p(stream)))
 
-    def rollout_device(self, state_in, state_out, in_ptrs, out_ptrs, plane, steps, e0, e1, device=0, stream=0):
+    def rollout_device(self, state_in, state_out, in_ptrs, out_ptrs, plane, steps, e0, e1, device=0, stream=0,
+                       record=True):
         """``steps`` closed-loop evaluations in one launch (``vsb_rollout_device``);
         raises ``_native.UnsupportedError`` when the plan has no such variant."""
         ins = (ctypes.c_void_p * max(1, len(in_ptrs)))(*in_ptrs)
         outs = (ctypes.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
         check(_native.lib().vsb_rollout_device(self._h, int(state_in), int(state_out), ins, outs, int(plane),
-                                               int(steps), int(e0), int(e1), int(device), ctypes.c_void_p(stream)))
+                                               int(steps), int(bool(record)), int(e0), int(e1), int(device),
+                                               ctypes.c_void_p(stream)))
 
     def eval_host(self, in_ptr, in_off, out_ptr, out_off, e0, e1, device=0):
         in_off = np.ascontiguousarray(in_off, dtype=np.int64)

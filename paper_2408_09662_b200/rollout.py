@@ -39,11 +39,13 @@ class Rollout:
     parameter row (bit patterns; ``rollout_batch`` broadcasts one theta,
     ``roa_scan`` has one per thrust limit) and gather; None = when at most half
     the rows are distinct.
+    ``record=False``: no trajectory -- ``traj`` is [2, B, n] (initial, final
+    state) and no other outputs are kept (``roa_scan``, quadsim.py:363-369).
     """
 
     def __init__(self, tape, batch: int, steps: int, *, state_in: int = 0, state_out: int = 0,
                  device=None, use_graph: bool = True, hoist=None, fused=None,
-                 dedup=None, **plan_options):
+                 dedup=None, record: bool = True, **plan_options):
         tape = as_tape(tape)
         if steps < 1:
             raise ValueError(f"steps must be >= 1, got {steps}")
@@ -67,12 +69,16 @@ class Rollout:
             self.pre_plan = None
             self.plan = get_plan(tape, **plan_options)
         B, dev = self.B, self.dev
-        self.traj = torch.zeros((steps + 1, B, n), dtype=torch.float64, device=dev)
+        self.record = bool(record)
+        self.traj = torch.zeros((steps + 1 if record else 2, B, n), dtype=torch.float64, device=dev)
         self.params = [None if i == state_in else torch.zeros((B, nz), dtype=torch.float64, device=dev)
                        for i, nz in enumerate(tape.nnz_in)]
         self.others = [j for j in range(tape.n_out) if j != state_out]
         self.outs = {j: torch.empty((steps, B, tape.nnz_out[j]), dtype=torch.float64, device=dev)
-                     for j in self.others}
+                     for j in self.others} if record else {}
+        if not record:   # step-loop fallback: ping-pong states, per-step scratch for the other outputs
+            self._pp = torch.empty((2, B, n), dtype=torch.float64, device=dev)
+            self._scr = {j: torch.empty((B, tape.nnz_out[j]), dtype=torch.float64, device=dev) for j in self.others}
         self.fused = fused is not False
         self.boundary = (torch.empty((B, self.split.boundary), dtype=torch.float64, device=dev)
                          if self.split is not None else None)
@@ -107,23 +113,32 @@ class Rollout:
             ins = [self.traj[0].data_ptr() if i == si else
                    (self.boundary.data_ptr() if self.split is not None else self.params[i].data_ptr())
                    for i in range(self.plan.tape.n_in)]
-            outs = [self.traj[1].data_ptr() if j == self.state_out else self.outs[j][0].data_ptr()
+            outs = [self.traj[1].data_ptr() if j == self.state_out or not self.record else self.outs[j][0].data_ptr()
                     for j in range(t.n_out)]
             try:
                 self.plan.rollout_device(si, self.state_out, ins, outs, self.B, self.steps, 0, self.B, dev,
-                                         s.cuda_stream)
+                                         s.cuda_stream, record=self.record)
                 return
             except UnsupportedError:
                 self.fused = False
         for k in range(self.steps):
             if self.split is not None:
-                ins = [self.traj[k].data_ptr(), self.boundary.data_ptr()]
+                ins = [self._state(k).data_ptr(), self.boundary.data_ptr()]
             else:
-                ins = [self.traj[k].data_ptr() if i == self.state_in else self.params[i].data_ptr()
+                ins = [self._state(k).data_ptr() if i == self.state_in else self.params[i].data_ptr()
                        for i in range(t.n_in)]
-            outs = [self.traj[k + 1].data_ptr() if j == self.state_out else self.outs[j][k].data_ptr()
+            outs = [self._state(k + 1).data_ptr() if j == self.state_out else self._out(j, k).data_ptr()
                     for j in range(t.n_out)]
             self.plan.eval_device_ptrs(ins, outs, 0, self.B, dev, s.cuda_stream)
+
+    def _state(self, k):
+        """state plane k of the step loop (record=False: ping-pong, the final one in traj[1])"""
+        if self.record or k == 0:
+            return self.traj[k]
+        return self.traj[1] if k == self.steps else self._pp[k % 2]
+
+    def _out(self, j, k):
+        return self.outs[j][k] if self.record else self._scr[j]
 
     @property
     def launches_per_run(self) -> int:

@@ -299,6 +299,29 @@ def test_hoisted_rollout_equals_unhoisted(name):
         assert_bitwise_or_nan(res[0][1][j], res[1][1][j], f"{name} out {j}")
 
 
+@pytest.mark.parametrize("name", ["pendulum", "quad_step"])
+@pytest.mark.parametrize("fused", [None, False])
+def test_rollout_without_trajectory(name, fused):
+    # roa_scan's mode (quadsim.py:363-369): only the final state is kept; same bits as
+    # the recorded trajectory's last plane
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape(name)
+    B, steps = 777, 9
+    ins = workloads.make_inputs(name, B, seed=37)
+    finals = []
+    for record in (True, False):
+        r = Rollout(tape, B, steps, record=record, fused=fused)
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
+        traj, outs = r.run()
+        assert fused is not None or r.fused
+        if not record:
+            assert traj.shape[0] == 2 and not outs
+            assert_bitwise_or_nan(traj[0].cpu().numpy(), ins[0], "initial state kept")
+        finals.append(traj[-1].cpu().numpy())
+    assert_bitwise_or_nan(finals[1], finals[0], f"{name} final state")
+
+
 @pytest.mark.parametrize("distinct", [1, 3])
 def test_rollout_dedup_of_parameter_rows(distinct):
     # rollout_batch broadcasts one theta, roa_scan has one per thrust limit: the hoisted

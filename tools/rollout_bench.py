@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--fused", choices=["auto", "off"], default="auto")
     ap.add_argument("--shared-theta", action="store_true", help="one parameter row for every env (rollout_batch's broadcast)")
     ap.add_argument("--dedup", choices=["auto", "off"], default="auto")
+    ap.add_argument("--no-record", action="store_true", help="final state only (roa_scan's mode)")
     args = ap.parse_args()
     tape = workloads.load_tape(args.workload)
     ins = workloads.make_inputs(args.workload, args.batch, seed=5)
@@ -42,7 +43,7 @@ def main():
     opts = {"team": args.team} if args.team else {}
     hoist = {"auto": None, "on": True, "off": False}[args.hoist]
     r = Rollout(tape, args.batch, args.steps, hoist=hoist, fused=None if args.fused == "auto" else False,
-                dedup=None if args.dedup == "auto" else False, **opts)
+                dedup=None if args.dedup == "auto" else False, record=not args.no_record, **opts)
     r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
     r.run()
     torch.cuda.synchronize()
@@ -73,7 +74,8 @@ def main():
                       "cpu_sample": f"{Bs} envs x {k_cpu} steps", "speedup": gpu_rate / cpu_rate,
                       "launches_per_rollout": r.launches_per_run, "plan": r.plan.info["team"],
                       "hoisted_rows": r.split.hoisted_rows if r.split is not None else 0, "fused": r.fused,
-                      "distinct_param_rows": r.u_count or None, "shared_theta": args.shared_theta}),
+                      "distinct_param_rows": r.u_count or None, "shared_theta": args.shared_theta,
+                      "record": not args.no_record}),
           flush=True)
 
 
