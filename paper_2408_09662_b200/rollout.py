@@ -24,6 +24,18 @@ from .tape import as_tape
 
 __all__ = ["Rollout", "rollout"]
 
+_SPLITS: dict = {}
+
+
+def _split_of(tape, state_in):
+    """split_invariant, memoised per (tape content, state input): the pass is O(rows) Python"""
+    key = (tape.digest() if callable(tape.digest) else tape.digest, state_in)
+    if key not in _SPLITS:
+        if len(_SPLITS) > 64:
+            _SPLITS.clear()
+        _SPLITS[key] = split_invariant(tape, (state_in,))
+    return _SPLITS[key]
+
 
 class Rollout:
     """A captured K-step rollout of ``state_{k+1} = tape(state_k, params)[state_out]``.
@@ -58,7 +70,7 @@ class Rollout:
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         if self.dev.index is None:
             self.dev = torch.device("cuda", torch.cuda.current_device())
-        self.split = split_invariant(tape, (state_in,)) if hoist is not False else None
+        self.split = _split_of(tape, state_in) if hoist is not False else None
         if hoist is None and self.split is not None and (
                 self.split.hoisted_rows < max(64, self.split.step_rows)):
             self.split = None
