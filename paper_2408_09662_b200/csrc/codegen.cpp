@@ -16,7 +16,8 @@
 namespace vsb {
 
 // operand counts, symcore.py:100-124
-static const int kArity[OP_COUNT] = {0, 0, 1, 1, 2, 2, 2, 2, 1, 1, 1, 2, 1, 1, 1, 1, 1, 2, 1, 2, 2, 1, 3};
+static const int kArity[OP_INTERNAL_END] = {0, 0, 1, 1, 2, 2, 2, 2, 1, 1, 1, 2, 1, 1, 1, 1, 1, 2, 1, 2, 2, 1, 3,
+                                            /* RCP */ 1, /* DIVR */ 3};
 
 int op_arity(int op) { return (op >= 0 && op < OP_COUNT) ? kArity[op] : -1; }
 
@@ -302,7 +303,8 @@ int op_cost(int op) {
     case OP_ADD: case OP_SUB: case OP_MUL: case OP_SQ: case OP_NEG: case OP_FABS: return 1;
     case OP_STEP: case OP_IF_ELSE: return 2;
     case OP_FMIN: case OP_FMAX: return 3;
-    case OP_DIV: return 10;
+    case OP_DIV: case OP_RCP: return 10;
+    case OP_DIVR: return 5;
     case OP_SQRT: return 8;
     case OP_EXP: case OP_LOG: return 25;
     case OP_SIN: case OP_COS: return 45;
@@ -701,6 +703,27 @@ void Emitter::build_header() {
     out_div = (opt.outline & 1) != 0;
     out_trig = (opt.outline & 2) != 0 && trig_exact;
     if (out_div) hdr.s += "__device__ __noinline__ real vs_div_o(real a, real b) { return a / b; }\n";
+    bool has_divr = false;
+    for (const Node& nd : p.nodes) has_divr |= nd.op == OP_DIVR;
+    if (has_divr)
+        // a / b from y = RN(1/b): q0 = RN(a y), one Newton correction brings q within 1 ulp,
+        // then Markstein's theorem (y within 1/2 ulp of 1/b, q within 1 ulp of a/b, FMA
+        // residual exact) makes RN(q + (a - b q) y) the correctly rounded quotient.  Valid with
+        // no underflow/overflow anywhere: y is NaN unless |b| in [2^-250, 2^250] and the result
+        // must land in [2^-250, 2^250] (so |a| is within 2^+-500); otherwise the IEEE division
+        hdr.s += "__device__ __noinline__ double vs_div_slow(double a, double b) { return a / b; }\n"
+                 "__device__ __noinline__ double vs_rcp_o(double b) {\n"
+                 "    const double ab = fabs(b);\n"
+                 "    return (ab >= 0x1p-250 && ab <= 0x1p250) ? 1.0 / b : __longlong_as_double(0x7ff8000000000000LL);\n}\n"
+                 "__device__ __forceinline__ double vs_divr(double a, double b, double y) {\n"
+                 "    double q = a * y;\n"
+                 "    double r = fma(-b, q, a);\n"
+                 "    q = fma(r, y, q);\n"
+                 "    r = fma(-b, q, a);\n"
+                 "    q = fma(r, y, q);\n"
+                 "    const unsigned e = ((unsigned)__double2hiint(q) >> 20) & 0x7ffu;\n"
+                 "    if (e - (1023u - 250u) > 500u) q = vs_div_slow(a, b);\n"
+                 "    return q;\n}\n";
     if (out_trig)
         hdr.s += "__device__ __noinline__ double vs_sin_o(double x) { return vs_sin(x); }\n"
                  "__device__ __noinline__ double vs_cos_o(double x) { return vs_cos(x); }\n"
@@ -729,6 +752,8 @@ std::string Emitter::expr_of(const Node& nd) const {
     case OP_SUB: snprintf(eb, sizeof eb, "%s - %s", X, Y); break;
     case OP_MUL: snprintf(eb, sizeof eb, "%s * %s", X, Y); break;
     case OP_DIV: snprintf(eb, sizeof eb, out_div ? "vs_div_o(%s, %s)" : "%s / %s", X, Y); break;
+    case OP_RCP: snprintf(eb, sizeof eb, "vs_rcp_o(%s)", X); break;
+    case OP_DIVR: snprintf(eb, sizeof eb, "vs_divr(%s, %s, %s)", X, Y, Z); break;
     case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
     case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
     case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
@@ -1604,6 +1629,61 @@ Kernelset Emitter::run() {
 
 }  // namespace
 
-Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) { return Emitter(p, opt, tag).run(); }
+// fp64 divisions by a shared divisor: one RCP node per divisor (a host-computed CONST when the
+// divisor is a constant) and DIVR nodes (a, b, y) in place of the DIVs.  Returns false when no
+// divisor is used twice.
+static bool rewrite_div(const Program& p, Program* out) {
+    const size_t N = p.nodes.size();
+    std::vector<int32_t> uses(N, 0);
+    for (const Node& nd : p.nodes)
+        if (nd.op == OP_DIV) ++uses[nd.arg[1]];
+    bool any = false;
+    for (int32_t u : uses) any |= u >= 2;
+    if (!any) return false;
+    Program q = p;
+    q.nodes.clear();
+    q.nodes.reserve(N + N / 8);
+    std::vector<int32_t> remap(N, -1), rcp(N, -1);
+    for (size_t i = 0; i < N; ++i) {
+        Node nd = p.nodes[i];
+        if (nd.op > OP_ASSIGN)
+            for (int k = 0; k < kArity[nd.op]; ++k) nd.arg[k] = remap[nd.arg[k]];
+        if (nd.op == OP_DIV && rcp[p.nodes[i].arg[1]] >= 0) {
+            nd.op = OP_DIVR;
+            nd.arg[2] = rcp[p.nodes[i].arg[1]];
+        }
+        remap[i] = static_cast<int32_t>(q.nodes.size());
+        q.nodes.push_back(nd);
+        if (uses[i] >= 2) {
+            Node r;
+            if (nd.op == OP_CONST) {
+                const double c = nd.imm, ac = std::fabs(c);
+                r.op = OP_CONST;
+                r.imm = (ac >= std::ldexp(1.0, -250) && ac <= std::ldexp(1.0, 250)) ? 1.0 / c : std::nan("");
+            } else {
+                r.op = OP_RCP;
+                r.arg[0] = remap[i];
+            }
+            rcp[i] = static_cast<int32_t>(q.nodes.size());
+            q.nodes.push_back(r);
+        }
+    }
+    for (Store& st : q.stores) st.node = remap[st.node];
+    *out = std::move(q);
+    return true;
+}
+
+Kernelset emit(const Program& p, const EmitOptions& opt, const std::string& tag) {
+    // off by default (VSB_DIV_RECIP=1 enables it): team kernels outline DIV (one shared
+    // subroutine, ~9 SASS instructions per call site) and are instruction-fetch bound --
+    // DIVR's inline correction + range check + fallback call grows srbm_mpc's code by 20 %
+    // (tools/sass_mix.py); thread-mode ldlt_12 / cartpole_rk4 gain nothing (1e6: 0.598 vs
+    // 0.567 ms, 0.0655 both; profiles/r1_sweeps_r65_divr.jsonl)
+    const char* env = getenv("VSB_DIV_RECIP");
+    const bool recip = env ? atoi(env) != 0 : opt.div_recip;
+    Program q;
+    if (recip && !opt.f32 && rewrite_div(p, &q)) return Emitter(q, opt, tag).run();
+    return Emitter(p, opt, tag).run();
+}
 
 }  // namespace vsb

@@ -20,7 +20,9 @@ namespace vsb {
 enum Op : uint8_t {
     OP_CONST = 0, OP_INPUT, OP_OUTPUT, OP_ASSIGN, OP_ADD, OP_SUB, OP_MUL, OP_DIV,
     OP_NEG, OP_EXP, OP_LOG, OP_POW, OP_SQRT, OP_SQ, OP_SIN, OP_COS, OP_TAN,
-    OP_ATAN2, OP_FABS, OP_FMIN, OP_FMAX, OP_STEP, OP_IF_ELSE, OP_COUNT
+    OP_ATAN2, OP_FABS, OP_FMIN, OP_FMAX, OP_STEP, OP_IF_ELSE, OP_COUNT,
+    // internal (never in a tape): RCP(b) = RN(1/b) (NaN outside 2^+-250); DIVR(a, b, RCP(b)) = a / b
+    OP_RCP = OP_COUNT, OP_DIVR, OP_INTERNAL_END
 };
 
 int op_arity(int op);
@@ -94,6 +96,10 @@ struct EmitOptions {
     // thread mode, single kernel: also emit `<name>_roll`, a K-step closed-loop kernel feeding
     // output `roll_out` back into input `roll_in` in registers (-1: none)
     int roll_in = -1, roll_out = -1;
+    // fp64: divisions sharing a divisor use one correctly rounded reciprocal and an FMA
+    // correction (Markstein) instead of a full division each; exact, with a fallback.
+    // Off by default (measured no faster); VSB_DIV_RECIP=1 turns it on
+    bool div_recip = false;
 };
 
 struct Chunk {
