@@ -569,6 +569,7 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     vsb_options_init(&p->opts);
     if (opts) p->opts = *opts;
     if (p->opts.dtype != VSB_F64 && p->opts.dtype != VSB_F32) return fail(VSB_ERR_INVALID, "unknown dtype");
+    const bool auto_block = p->opts.block <= 0;
     if (p->opts.block <= 0) p->opts.block = 128;
     if (p->opts.block % 32 != 0 || p->opts.block > 1024) return fail(VSB_ERR_INVALID, "block must be a multiple of 32 in [32, 1024]");
     const bool auto_min_blocks = p->opts.min_blocks <= 0;
@@ -595,6 +596,16 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     // 0.033 ms; profiles/r1_sweeps_r19.jsonl)
     if (auto_min_blocks && p->opts.team == 0 && p->opts.block == 128 && p->prog.n_live_ops <= 600)
         p->opts.min_blocks = 8;
+    // thread mode, wide I/O rows: 64-instance tiles when two 128-instance tiles of the TMA
+    // pipeline would not fit in shared memory (ldlt_12, 816 B per instance, B=1e6: block 128
+    // 0.567 ms (no TMA) -> block 64 + TMA 0.350 ms; profiles/r1_sweeps_r66_ldlt12_block.jsonl)
+    if (auto_block && p->opts.team == 0) {
+        int64_t io = 0;
+        for (auto x : p->prog.nnz_in) io += x;
+        for (auto x : p->prog.nnz_out) io += x;
+        io *= p->rsz();
+        if (2 * io * 128 + 64 > 200 * 1024 && 2 * io * 64 + 64 <= 200 * 1024) p->opts.block = 64;
+    }
     if (p->opts.groups < 0 || p->opts.groups > 32) return fail(VSB_ERR_INVALID, "groups must be in [0, 32]");
     if (p->opts.cluster < 0 || p->opts.cluster > 16) return fail(VSB_ERR_INVALID, "cluster must be in [0, 16]");
     if (p->opts.groups == 0) p->opts.groups = 1;
