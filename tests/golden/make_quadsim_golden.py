@@ -40,6 +40,15 @@ def main():
     um = np.array([2.0, 4.905, 8.0])
     masks = quadsim.roa_scan(mx, mw, um, steps=200, tape=tape, n_threads=2)
     out.update(roa_mx=mx, roa_mw=mw, roa_um=um, roa_masks=np.stack(masks))
+    rows = quadsim.param_sweep("mass", [0.4, 0.5, 0.7], steps=30, tape=tape, n_threads=1)
+    out.update(ps_values=np.array([r[1] for r in rows]), ps_steps=np.array([r[2] for r in rows]),
+               ps_data=np.array([r[3:] for r in rows]))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        quadsim.write_roa_csv(os.path.join(d, "roa.csv"), um, mx, mw, masks)
+        quadsim.write_sweep_csv(os.path.join(d, "sweep.csv"), rows[:7])
+        out.update(roa_csv=np.array(open(os.path.join(d, "roa.csv")).read()),
+                   sweep_csv=np.array(open(os.path.join(d, "sweep.csv")).read()))
     np.savez_compressed(os.path.join(HERE, "quadsim.npz"), **out)
     print({k: v.shape for k, v in out.items()}, "stable frac", float(np.stack(masks).mean()))
 

@@ -76,3 +76,25 @@ def test_roa_scan_matches_reference(golden):
                         tape=workloads.load_tape("quad_step"))
     assert len(masks) == 3
     np.testing.assert_array_equal(np.stack(masks), golden["roa_masks"])
+
+
+def test_csv_writers_match_reference(golden, tmp_path):
+    masks = list(golden["roa_masks"])
+    qs.write_roa_csv(tmp_path / "roa.csv", golden["roa_um"], golden["roa_mx"], golden["roa_mw"], masks)
+    assert (tmp_path / "roa.csv").read_text() == str(golden["roa_csv"])
+    rows = [("mass", float(v), int(k), *d) for v, k, d in zip(golden["ps_values"][:7], golden["ps_steps"][:7],
+                                                                golden["ps_data"][:7])]
+    qs.write_sweep_csv(tmp_path / "sweep.csv", rows)
+    assert (tmp_path / "sweep.csv").read_text() == str(golden["sweep_csv"])
+    with pytest.raises(ValueError):
+        qs.write_roa_csv(tmp_path / "x.csv", [1.0, 2.0], golden["roa_mx"], golden["roa_mw"], masks[:1])
+
+
+@pytest.mark.gpu
+def test_param_sweep_matches_reference(golden):
+    rows = qs.param_sweep("mass", [0.4, 0.5, 0.7], steps=30, tape=workloads.load_tape("quad_step"))
+    assert len(rows) == golden["ps_data"].shape[0]
+    assert all(r[0] == "mass" for r in rows)
+    np.testing.assert_array_equal([r[1] for r in rows], golden["ps_values"])
+    np.testing.assert_array_equal([r[2] for r in rows], golden["ps_steps"])
+    assert_close(np.array([r[3:] for r in rows]), golden["ps_data"], RTOL64 * 50, "sweep rows")
