@@ -59,7 +59,9 @@ def main():
                       "piece_bytes": os.environ.get("VSB_HOST_PIECE_BYTES", "default"),
                       "ms_median": 1e3 * float(np.median(t)), "ms_min": 1e3 * min(t),
                       "evals_per_s": args.batch / float(np.median(t)), "h2d_gbs": h2d, "d2h_gbs": d2h,
-                      "in_bytes": nbytes, "out_bytes": ws._out_buf.nbytes}))
+                      "in_bytes": nbytes, "out_bytes": ws._out_buf.nbytes,
+                      "zc_out": os.environ.get("VSB_ZC_OUT", "default"),
+                      "out_sha": __import__("hashlib").sha256(ws._out_buf.tobytes()).hexdigest()[:16]}))
 
 
 if __name__ == "__main__":
