@@ -15,6 +15,7 @@ resident boundary buffer -- bit for bit the same trajectory.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from ._native import UnsupportedError
@@ -81,18 +82,20 @@ class Rollout:
             self.pre_plan = None
             self.plan = get_plan(tape, **plan_options)
         B, dev = self.B, self.dev
+        # fp32 plans (dtype="float32") roll out in float32 buffers
+        self.dt = torch.float32 if self.plan.np_dtype == np.float32 else torch.float64
         self.record = bool(record)
-        self.traj = torch.zeros((steps + 1 if record else 2, B, n), dtype=torch.float64, device=dev)
-        self.params = [None if i == state_in else torch.zeros((B, nz), dtype=torch.float64, device=dev)
+        self.traj = torch.zeros((steps + 1 if record else 2, B, n), dtype=self.dt, device=dev)
+        self.params = [None if i == state_in else torch.zeros((B, nz), dtype=self.dt, device=dev)
                        for i, nz in enumerate(tape.nnz_in)]
         self.others = [j for j in range(tape.n_out) if j != state_out]
-        self.outs = {j: torch.empty((steps, B, tape.nnz_out[j]), dtype=torch.float64, device=dev)
+        self.outs = {j: torch.empty((steps, B, tape.nnz_out[j]), dtype=self.dt, device=dev)
                      for j in self.others} if record else {}
         if not record:   # step-loop fallback: ping-pong states, per-step scratch for the other outputs
-            self._pp = torch.empty((2, B, n), dtype=torch.float64, device=dev)
-            self._scr = {j: torch.empty((B, tape.nnz_out[j]), dtype=torch.float64, device=dev) for j in self.others}
+            self._pp = torch.empty((2, B, n), dtype=self.dt, device=dev)
+            self._scr = {j: torch.empty((B, tape.nnz_out[j]), dtype=self.dt, device=dev) for j in self.others}
         self.fused = fused is not False
-        self.boundary = (torch.empty((B, self.split.boundary), dtype=torch.float64, device=dev)
+        self.boundary = (torch.empty((B, self.split.boundary), dtype=self.dt, device=dev)
                          if self.split is not None else None)
         self.use_graph, self.dedup = use_graph, dedup
         self.u_count, self.u_params, self.u_boundary = 0, None, None
@@ -163,28 +166,29 @@ class Rollout:
             params.insert(self.state_in, None)
         if len(params) != self.tape.n_in:
             raise ValueError(f"expected {self.tape.n_in - 1} parameter inputs")
-        self.traj[0].copy_(torch.as_tensor(state0, dtype=torch.float64))
+        self.traj[0].copy_(torch.as_tensor(state0, dtype=self.dt))
         for i, p in enumerate(params):
             if i != self.state_in:
-                self.params[i].copy_(torch.as_tensor(p, dtype=torch.float64))
+                self.params[i].copy_(torch.as_tensor(p, dtype=self.dt))
         if self.split is not None and self.split.fixed and self.dedup is not False:
             self._dedup()
 
     def _dedup(self):
         fixed = self.split.fixed
-        rows = torch.cat([self.params[i] for i in fixed], 1).contiguous().view(torch.int64)
+        ity = torch.int32 if self.dt == torch.float32 else torch.int64
+        rows = torch.cat([self.params[i] for i in fixed], 1).contiguous().view(ity)
         uniq, inv = torch.unique(rows, dim=0, return_inverse=True)   # by bit pattern: +-0 and NaNs kept apart
         U = int(uniq.shape[0])
         if self.dedup is None and 2 * U > self.B:
             if self.u_count:
                 self.u_count, self.graph = 0, None
             return
-        uniq = uniq.view(torch.float64)
+        uniq = uniq.view(self.dt)
         if U != self.u_count:
             self.u_count, self.graph = U, None
-            self.u_params = [torch.empty((U, self.tape.nnz_in[i]), dtype=torch.float64, device=self.dev)
+            self.u_params = [torch.empty((U, self.tape.nnz_in[i]), dtype=self.dt, device=self.dev)
                              for i in fixed]
-            self.u_boundary = torch.empty((U, self.split.boundary), dtype=torch.float64, device=self.dev)
+            self.u_boundary = torch.empty((U, self.split.boundary), dtype=self.dt, device=self.dev)
         col = 0
         for p, i in zip(self.u_params, fixed):
             nz = self.tape.nnz_in[i]

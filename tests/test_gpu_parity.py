@@ -322,6 +322,24 @@ def test_rollout_without_trajectory(name, fused):
     assert_bitwise_or_nan(finals[1], finals[0], f"{name} final state")
 
 
+@pytest.mark.parametrize("name", ["pendulum", "quad_step"])
+def test_fp32_rollout_fused_equals_loop(name):
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape(name)
+    B, steps = 513, 7
+    ins = workloads.make_inputs(name, B, seed=41)
+    res = []
+    for fused in (None, False):
+        r = Rollout(tape, B, steps, fused=fused, dtype="float32")
+        assert r.traj.dtype == torch.float32
+        r.set(torch.tensor(ins[0], device="cuda"), [torch.tensor(v, device="cuda") for v in ins[1:]])
+        traj, _ = r.run()
+        res.append(traj.cpu().numpy())
+    assert_bitwise_or_nan(res[0], res[1], f"{name} fp32 traj")
+    assert np.abs(res[0][1] - ins[0]).max() < 10.0   # one step stays near the start
+
+
 @pytest.mark.parametrize("distinct", [1, 3])
 def test_rollout_dedup_of_parameter_rows(distinct):
     # rollout_batch broadcasts one theta, roa_scan has one per thrust limit: the hoisted
