@@ -268,7 +268,38 @@ def secondary_points(dev, local, hbm_gbs, steps=5):
                     "hbm_gbs": gbs, "hbm_frac": gbs / hbm_gbs, "team": info["team"], "n_chunks": info["n_chunks"],
                     "max_rel_err_16_rows": worst})
         del d_in, d_out
+    out.append(rollout_point(dev))
     return out
+
+
+def rollout_point(dev, B=10000, K=100, reps=5):
+    """quadsim.rollout_batch's closed loop (quad_step, one broadcast
+    theta) as one device-resident rollout -- hoisted pre tape + fused K-step kernel."""
+    import torch
+
+    import workloads
+    from paper_2408_09662_b200.rollout import Rollout
+
+    tape = workloads.load_tape("quad_step")
+    ins = workloads.make_inputs("quad_step", B, seed=2001)
+    theta = np.repeat(ins[1][:1], B, axis=0)
+    r = Rollout(tape, B, K, device=dev)
+    r.set(torch.tensor(ins[0], device=dev), [torch.tensor(theta, device=dev)])
+    r.run()
+    torch.cuda.synchronize(dev)
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r.run()
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = statistics.median(ms) / 1e3
+    return {"workload": "quad_step rollout (quadsim.rollout_batch, one theta)", "batch": B, "steps": K,
+            "value": B * K / t, "unit": "env-steps/s", "ms_per_rollout": t * 1e3,
+            "hoisted_rows": r.split.hoisted_rows if r.split is not None else 0, "fused": r.fused,
+            "launches_per_rollout": r.launches_per_run}
 
 
 def run_ours(args):
