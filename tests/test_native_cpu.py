@@ -135,3 +135,24 @@ def test_auto_team_width_follows_the_scheduled_live_set():
     for name, team in want.items():
         p = Plan(workloads.load_tape(name), cache_dir="", compile_threads=-1)
         assert p.info["team"] == team, name
+
+
+def test_rollout_device_argument_errors_without_gpu():
+    # vsb_rollout_device validates before touching the device (ValueError like the reference)
+    plan = Plan(workloads.load_tape("pendulum"), compile_threads=-1)
+    ptrs = [0] * 2
+    with pytest.raises(ValueError, match="out of range"):
+        plan.rollout_device(5, 0, ptrs, ptrs, 10, 3, 0, 10)
+    with pytest.raises(ValueError, match="sizes differ"):
+        plan.rollout_device(1, 1, ptrs, ptrs, 10, 3, 0, 10)   # 3 parameters vs 1 energy output
+    with pytest.raises(ValueError, match="plane"):
+        plan.rollout_device(0, 0, ptrs, ptrs, 5, 3, 0, 10)
+
+
+def test_hoisted_split_is_memoised():
+    from paper_2408_09662_b200 import rollout
+
+    t = workloads.load_tape("quad_step")
+    a = rollout._split_of(t, 0)
+    assert rollout._split_of(workloads.load_tape("quad_step"), 0) is a
+    assert a.hoisted_rows == 42501
