@@ -519,7 +519,7 @@ private:
     void emit_store(Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) const;
     void input_load(Out& o, int32_t u, const char* ind) const;
     void io_bases(Out& o) const;
-    void emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll = false) const;
+    void emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll = false, bool roll_hoisted = false) const;
     bool roll_possible() const;
     void emit_roll_kernel(Chunk& ch, Out& b) const;
     void emit_thread_chunk(int c, Chunk& ch, Out& b);
@@ -837,7 +837,7 @@ void Emitter::io_bases(Out& o) const {
         for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
 }
 
-void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll) const {
+void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll, bool roll_hoisted) const {
     // ops of the chunk with direct I/O: inputs `I<i>[k]` (smem tile row) or `__ldg(I<i> + k)`
     // (global row), outputs `O<j>[k] = v`; one thread per instance, no scratch.  `roll`: the
     // state input `opt.roll_in` reads registers `st<k>`, stores to `opt.roll_out` also set `nt<k>`
@@ -847,6 +847,7 @@ void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll) con
         const Node& nu = p.nodes[u];
         if (nu.op != OP_INPUT || got[u]) return;
         got[u] = 1;
+        if (roll_hoisted && nu.in_i != opt.roll_in) return;   // loaded once before the step loop
         if (roll && nu.in_i == opt.roll_in) b.put("%sconst real v%d = st%d;\n", ind, u, nu.in_k);
         else if (ldg) b.put("%sconst real v%d = __ldg(I%d + %d);\n", ind, u, nu.in_i, nu.in_k);
         else b.put("%sconst real v%d = I%d[%d];\n", ind, u, nu.in_i, nu.in_k);
@@ -902,10 +903,19 @@ void Emitter::emit_roll_kernel(Chunk& ch, Out& b) const {
     for (int j = 0; j < n_out; ++j)
         b.put("    real* __restrict__ O%d = A.out[%d] + e * %" PRId64 "LL;\n", j, j, p.nnz_out[j]);
     for (int64_t k = 0; k < n; ++k) b.put("    real st%" PRId64 " = __ldg(I%d + %" PRId64 ");\n", k, opt.roll_in, k);
+    // the other inputs are the same every step: load them once (when few enough to stay in
+    // registers) instead of once per step (ncu: long-scoreboard + LSU-throttle stalls)
+    std::vector<int32_t> fixed_in;
+    for (int64_t q = 0; q < N; ++q)
+        if (p.nodes[q].op == OP_INPUT && p.nodes[q].in_i != opt.roll_in) fixed_in.push_back(static_cast<int32_t>(q));
+    const bool hoisted = fixed_in.size() <= 64;
+    if (hoisted)
+        for (int32_t u : fixed_in)
+            b.put("    const real v%d = __ldg(I%d + %d);\n", u, p.nodes[u].in_i, p.nodes[u].in_k);
     b.put("    const bool rec = A.io_ld == 0;\n");
     b.put("    for (long long step = 0; step < A.ld; ++step) {\n");
     for (int64_t k = 0; k < n; ++k) b.put("        real nt%" PRId64 ";\n", k);
-    emit_direct_body(b, ch, true, true);
+    emit_direct_body(b, ch, true, true, hoisted);
     for (int64_t k = 0; k < n; ++k) b.put("        st%" PRId64 " = nt%" PRId64 ";\n", k, k);
     b.put("        if (rec) {\n");
     for (int j = 0; j < n_out; ++j) b.put("            O%d += A.ipc * %" PRId64 "LL;\n", j, p.nnz_out[j]);
