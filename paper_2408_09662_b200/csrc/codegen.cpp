@@ -519,7 +519,8 @@ private:
     void emit_store(Out& o, int32_t s_idx, const std::string& val, const char* ind, bool staged) const;
     void input_load(Out& o, int32_t u, const char* ind) const;
     void io_bases(Out& o) const;
-    void emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll = false, bool roll_hoisted = false) const;
+    void emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll = false, bool roll_hoisted = false,
+                          const std::vector<uint8_t>* roll_vec = nullptr) const;
     bool roll_possible() const;
     void emit_roll_kernel(Chunk& ch, Out& b) const;
     void emit_thread_chunk(int c, Chunk& ch, Out& b);
@@ -837,7 +838,8 @@ void Emitter::io_bases(Out& o) const {
         for (int j = 0; j < n_out; ++j) o.put("    (void)O%d;\n", j);
 }
 
-void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll, bool roll_hoisted) const {
+void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll, bool roll_hoisted,
+                               const std::vector<uint8_t>* roll_vec) const {
     // ops of the chunk with direct I/O: inputs `I<i>[k]` (smem tile row) or `__ldg(I<i> + k)`
     // (global row), outputs `O<j>[k] = v`; one thread per instance, no scratch.  `roll`: the
     // state input `opt.roll_in` reads registers `st<k>`, stores to `opt.roll_out` also set `nt<k>`
@@ -854,7 +856,10 @@ void Emitter::emit_direct_body(Out& b, const Chunk& ch, bool ldg, bool roll, boo
     };
     auto store = [&](size_t si, const std::string& val) {
         const Store& st = p.stores[si];
-        b.put(roll ? "%sif (rec) O%d[%d] = %s;\n" : "%sO%d[%d] = %s;\n", ind, st.j, st.k, val.c_str());
+        if (roll_vec && (*roll_vec)[st.j])   // stored after the step with 16-byte vectors
+            b.put("%sot%d_%d = %s;\n", ind, st.j, st.k, val.c_str());
+        else
+            b.put(roll ? "%sif (rec) O%d[%d] = %s;\n" : "%sO%d[%d] = %s;\n", ind, st.j, st.k, val.c_str());
         if (roll && st.j == opt.roll_out) b.put("%snt%d = %s;\n", ind, st.k, val.c_str());
     };
     for (size_t si = 0; si < p.stores.size(); ++si) {
@@ -913,11 +918,48 @@ void Emitter::emit_roll_kernel(Chunk& ch, Out& b) const {
         for (int32_t u : fixed_in)
             b.put("    const real v%d = __ldg(I%d + %d);\n", u, p.nodes[u].in_i, p.nodes[u].in_k);
     b.put("    const bool rec = A.io_ld == 0;\n");
+    // recorded outputs whose rows are whole 16-byte vectors and fully stored leave at the
+    // end of each step as vector stores (one STG.128 per 16 bytes instead of per element)
+    const int V = 16 / rsz;
+    std::vector<uint8_t> vec(n_out, 0);
+    std::vector<int64_t> cover(n_out, 0);
+    for (const Store& st : p.stores) ++cover[st.j];
+    bool any_vec = false;
+    for (int j = 0; j < n_out; ++j) {
+        vec[j] = p.nnz_out[j] > 0 && p.nnz_out[j] % V == 0 && cover[j] == p.nnz_out[j];
+        any_vec |= vec[j] != 0;
+    }
+    if (any_vec) {
+        b.put("    const bool va = true");
+        for (int j = 0; j < n_out; ++j)
+            if (vec[j]) b.put(" && ((reinterpret_cast<unsigned long long>(A.out[%d]) & 15ULL) == 0)", j);
+        b.put(";\n");
+    }
     b.put("    for (long long step = 0; step < A.ld; ++step) {\n");
     for (int64_t k = 0; k < n; ++k) b.put("        real nt%" PRId64 ";\n", k);
-    emit_direct_body(b, ch, true, true, hoisted);
+    for (int j = 0; j < n_out; ++j)
+        if (vec[j])
+            for (int64_t k = 0; k < p.nnz_out[j]; ++k) b.put("        real ot%d_%" PRId64 ";\n", j, k);
+    emit_direct_body(b, ch, true, true, hoisted, any_vec ? &vec : nullptr);
     for (int64_t k = 0; k < n; ++k) b.put("        st%" PRId64 " = nt%" PRId64 ";\n", k, k);
     b.put("        if (rec) {\n");
+    if (any_vec) {
+        b.put("            if (va) {\n");
+        for (int j = 0; j < n_out; ++j) {
+            if (!vec[j]) continue;
+            for (int64_t k = 0; k < p.nnz_out[j]; k += V) {
+                b.put("                *reinterpret_cast<vec_t*>(O%d + %" PRId64 ") = vec_t{", j, k);
+                for (int u = 0; u < V; ++u) b.put(u ? ", ot%d_%" PRId64 : "ot%d_%" PRId64, j, k + u);
+                b.put("};\n");
+            }
+        }
+        b.put("            } else {\n");
+        for (int j = 0; j < n_out; ++j)
+            if (vec[j])
+                for (int64_t k = 0; k < p.nnz_out[j]; ++k)
+                    b.put("                O%d[%" PRId64 "] = ot%d_%" PRId64 ";\n", j, k, j, k);
+        b.put("            }\n");
+    }
     for (int j = 0; j < n_out; ++j) b.put("            O%d += A.ipc * %" PRId64 "LL;\n", j, p.nnz_out[j]);
     b.put("        }\n    }\n    if (!rec) {\n");
     for (int64_t k = 0; k < n; ++k) b.put("        O%d[%" PRId64 "] = st%" PRId64 ";\n", opt.roll_out, k, k);
