@@ -18,7 +18,7 @@ from __future__ import annotations
 import csv
 import statistics
 import time
-from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 
@@ -34,8 +34,10 @@ _MAX_INNER_CALLS = 1_000_000_000
 CSV_HEADER = ("n_instructions", "batch_size", "n_threads", "t_serial_total", "t_batch", "speedup")
 
 
-@dataclass(frozen=True)
-class BenchRecord:
+class BenchRecord(NamedTuple):
+    """One (case, batch) row of bench.csv: the reference's six columns (``speedup``
+    derived, bench.py:1-9) plus ``repetitions`` and the optional device-only time."""
+
     n_instructions: int
     batch_size: int
     n_threads: int
@@ -44,36 +46,36 @@ class BenchRecord:
     repetitions: int
     t_device: float | None = None
 
-    def __post_init__(self):
-        if not (self.t_serial_total > 0 and self.t_batch > 0):
-            raise ValueError("timings must be positive")
-
     @property
     def speedup(self) -> float:
         return self.t_serial_total / self.t_batch
 
 
+def _record(*fields, **kw) -> BenchRecord:
+    rec = BenchRecord(*fields, **kw)
+    if rec.t_serial_total <= 0 or rec.t_batch <= 0:
+        raise ValueError("timings must be positive")
+    return rec
+
+
 def _median_call_time(fn, repetitions: int) -> float:
-    """Median per-call seconds; loops fast calls until the timer resolves (bench.py:133-156)."""
-    floor = time.get_clock_info("perf_counter").resolution * _MIN_TIMER_TICKS
-    inner = 1
-    while True:
-        start = time.perf_counter()
-        for _ in range(inner):
+    """Median seconds per call over ``repetitions`` samples; each sample runs the call
+    enough times (a power of ten) to span >= 100 ticks of the host timer."""
+    need = time.get_clock_info("perf_counter").resolution * _MIN_TIMER_TICKS
+
+    def sample(calls: int) -> float:
+        t0 = time.perf_counter()
+        for _ in range(calls):
             fn()
-        elapsed = time.perf_counter() - start
-        if elapsed >= floor:
-            break
-        if inner >= _MAX_INNER_CALLS:
-            raise RuntimeError(f"timer resolution insufficient: {inner} calls span {elapsed:.3e}s < {floor:.3e}s")
-        inner *= 10
-    samples = [elapsed / inner]
-    for _ in range(repetitions - 1):
-        start = time.perf_counter()
-        for _ in range(inner):
-            fn()
-        samples.append((time.perf_counter() - start) / inner)
-    return statistics.median(samples)
+        return time.perf_counter() - t0
+
+    calls, first = 1, sample(1)
+    while first < need:
+        if calls >= _MAX_INNER_CALLS:
+            raise RuntimeError(f"timer resolution insufficient: {calls} calls span {first:.3e}s < {need:.3e}s")
+        calls *= 10
+        first = sample(calls)
+    return statistics.median([first / calls] + [sample(calls) / calls for _ in range(repetitions - 1)])
 
 
 def _device_time(tape, ws: BatchWorkspace, repetitions: int, device: int) -> float:
@@ -140,7 +142,7 @@ def run_benchmark(cases, batch_sizes, n_threads: int | None = None, repetitions:
                 batch_eval(tape, ws, n_threads=n_threads, device=device)
             t_batch = _median_call_time(lambda: batch_eval(tape, ws, n_threads=n_threads, device=device), repetitions)
             t_dev = _device_time(tape, ws, repetitions, device) if device_column else None
-            records.append(BenchRecord(tape.n_arith, batch, n_threads, batch * t_serial, t_batch, repetitions, t_dev))
+            records.append(_record(tape.n_arith, batch, n_threads, batch * t_serial, t_batch, repetitions, t_dev))
     return records
 
 

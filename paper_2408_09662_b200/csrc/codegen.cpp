@@ -116,11 +116,30 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
     }
     // ASSIGN rows count as arithmetic in nothing (bench.py:50-52); others already counted
 
+    // output nonzeros no OUTPUT row writes: the reference's run_range leaves them untouched
+    // in its np.zeros-initialised BatchWorkspace (batchrt.py:116), so they read 0.0; device
+    // buffers here are reused, so each such nonzero gets an explicit store of +0.0
+    int32_t zero_node = -1;
+    for (int j = 0; j < n_out && zero_node < 0; ++j)
+        for (auto id : stored[j])
+            if (id < 0) {
+                auto it = const_node.find(0);   // bit pattern of +0.0
+                if (it == const_node.end()) {
+                    Node z;
+                    z.op = OP_CONST;
+                    z.imm = 0.0;
+                    nodes.push_back(z);
+                    it = const_node.emplace(0, static_cast<int32_t>(nodes.size() - 1)).first;
+                }
+                zero_node = it->second;
+                break;
+            }
     // dead-code elimination: only values reaching an output store survive
     const size_t N = nodes.size();
     std::vector<uint8_t> live(N, 0);
     for (int j = 0; j < n_out; ++j)
         for (auto id : stored[j]) if (id >= 0) live[id] = 1;
+    if (zero_node >= 0) live[zero_node] = 1;
     for (size_t q = N; q-- > 0;) {
         if (!live[q]) continue;
         const Node& nd = nodes[q];
@@ -144,6 +163,7 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
     for (int j = 0; j < n_out; ++j)
         for (int64_t k = 0; k < p.nnz_out[j]; ++k)
             if (stored[j][k] >= 0) p.stores.push_back({j, static_cast<int32_t>(k), remap[stored[j][k]]});
+            else { p.stores.push_back({j, static_cast<int32_t>(k), remap[zero_node]}); ++p.n_zero_stores; }
 
     p.in_base.assign(n_in + 1, 0);
     for (int i = 0; i < n_in; ++i) p.in_base[i + 1] = p.in_base[i] + p.nnz_in[i];
@@ -493,7 +513,7 @@ private:
     const EmitOptions& opt;
     const std::string& tag;
     Kernelset ks;
-    bool team = false, f32 = false, soa = false, trig_exact = false, out_div = false, out_trig = false;
+    bool team = false, f32 = false, soa = false, trig_exact = false, out_div = false, out_trig = false, out_tr = false;
     int64_t N = 0;
     int n_in = 0, n_out = 0, rsz = 8;
     const char* real = "double";
@@ -703,6 +723,19 @@ void Emitter::build_header() {
     }
     out_div = (opt.outline & 1) != 0;
     out_trig = (opt.outline & 2) != 0 && trig_exact;
+    out_tr = (opt.outline & 4) != 0;
+    if (out_tr)
+        // libdevice transcendentals as shared subroutines: a tape with hundreds of them
+        // otherwise inlines ~100 SASS per use (and ptxas time grows superlinearly)
+        hdr.put("__device__ __noinline__ real vs_exp_o(real x) { return exp%s(x); }\n"
+                "__device__ __noinline__ real vs_log_o(real x) { return log%s(x); }\n"
+                "__device__ __noinline__ real vs_pow_o(real x, real y) { return pow%s(x, y); }\n"
+                "__device__ __noinline__ real vs_tan_o(real x) { return tan%s(x); }\n"
+                "__device__ __noinline__ real vs_atan2_o(real x, real y) { return atan2%s(x, y); }\n",
+                fs, fs, fs, fs, fs);
+    if (out_tr && !trig_exact)
+        hdr.put("__device__ __noinline__ real vs_sin_l(real x) { return sin%s(x); }\n"
+                "__device__ __noinline__ real vs_cos_l(real x) { return cos%s(x); }\n", fs, fs);
     if (out_div) hdr.s += "__device__ __noinline__ real vs_div_o(real a, real b) { return a / b; }\n";
     bool has_divr = false;
     for (const Node& nd : p.nodes) has_divr |= nd.op == OP_DIVR;
@@ -756,21 +789,23 @@ std::string Emitter::expr_of(const Node& nd) const {
     case OP_RCP: snprintf(eb, sizeof eb, "vs_rcp_o(%s)", X); break;
     case OP_DIVR: snprintf(eb, sizeof eb, "vs_divr(%s, %s, %s)", X, Y, Z); break;
     case OP_NEG: snprintf(eb, sizeof eb, "-%s", X); break;
-    case OP_EXP: snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
-    case OP_LOG: snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
-    case OP_POW: snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
+    case OP_EXP: if (out_tr) snprintf(eb, sizeof eb, "vs_exp_o(%s)", X); else snprintf(eb, sizeof eb, "exp%s(%s)", fs, X); break;
+    case OP_LOG: if (out_tr) snprintf(eb, sizeof eb, "vs_log_o(%s)", X); else snprintf(eb, sizeof eb, "log%s(%s)", fs, X); break;
+    case OP_POW: if (out_tr) snprintf(eb, sizeof eb, "vs_pow_o(%s, %s)", X, Y); else snprintf(eb, sizeof eb, "pow%s(%s, %s)", fs, X, Y); break;
     case OP_SQRT: snprintf(eb, sizeof eb, "sqrt%s(%s)", fs, X); break;
     case OP_SQ: snprintf(eb, sizeof eb, "%s * %s", X, X); break;
     case OP_SIN:
         if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_sin_o(%s)" : "vs_sin(%s)", X);
+        else if (out_tr) snprintf(eb, sizeof eb, "vs_sin_l(%s)", X);
         else snprintf(eb, sizeof eb, "sin%s(%s)", fs, X);
         break;
     case OP_COS:
         if (trig_exact) snprintf(eb, sizeof eb, out_trig ? "vs_cos_o(%s)" : "vs_cos(%s)", X);
+        else if (out_tr) snprintf(eb, sizeof eb, "vs_cos_l(%s)", X);
         else snprintf(eb, sizeof eb, "cos%s(%s)", fs, X);
         break;
-    case OP_TAN: snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
-    case OP_ATAN2: snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
+    case OP_TAN: if (out_tr) snprintf(eb, sizeof eb, "vs_tan_o(%s)", X); else snprintf(eb, sizeof eb, "tan%s(%s)", fs, X); break;
+    case OP_ATAN2: if (out_tr) snprintf(eb, sizeof eb, "vs_atan2_o(%s, %s)", X, Y); else snprintf(eb, sizeof eb, "atan2%s(%s, %s)", fs, X, Y); break;
     case OP_FABS: snprintf(eb, sizeof eb, "fabs%s(%s)", fs, X); break;
     case OP_FMIN: snprintf(eb, sizeof eb, "vs_fmin(%s, %s)", X, Y); break;
     case OP_FMAX: snprintf(eb, sizeof eb, "vs_fmax(%s, %s)", X, Y); break;

@@ -48,6 +48,7 @@ struct Program {
     int64_t n_arith_rows = 0;     // rows other than CONST/INPUT/OUTPUT/ASSIGN
     int64_t n_live_ops = 0;       // live arithmetic SSA values after DCE
     int64_t n_dead = 0;           // arithmetic values removed by DCE
+    int64_t n_zero_stores = 0;    // output nonzeros no OUTPUT row writes (stored as +0.0)
 };
 
 // Build the SSA program from the packed tape (the run_range argument set).

@@ -281,7 +281,24 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.groups = p->opts.groups;
     eo.cluster = p->opts.cluster;
     eo.bulk_io = p->opts.bulk_io >= 0 && !roll;
-    eo.outline = p->opts.outline < 0 ? 0 : (p->opts.outline == 0 ? (eo.team >= 2 ? 3 : 0) : p->opts.outline);
+    // outlined subroutines (bit 0 DIV, bit 1 SIN/COS, bit 2 EXP/LOG/POW/TAN/ATAN2): team kernels
+    // are instruction-fetch bound and outline DIV + SIN/COS; any plan outlines SIN/COS and the
+    // libdevice transcendentals once a tape has more than 48 of them (inlined, each costs
+    // ~100-250 SASS and NVRTC/ptxas time grows superlinearly: a 3000-row fuzz tape with 900
+    // transcendentals took minutes to compile)
+    if (p->opts.outline == 0) {
+        int64_t n_trig = 0, n_tr = 0;
+        for (const auto& nd : p->prog.nodes) {
+            n_trig += nd.op == vsb::OP_SIN || nd.op == vsb::OP_COS;
+            n_tr += nd.op == vsb::OP_EXP || nd.op == vsb::OP_LOG || nd.op == vsb::OP_POW || nd.op == vsb::OP_TAN ||
+                    nd.op == vsb::OP_ATAN2;
+        }
+        eo.outline = eo.team >= 2 ? 3 : 0;
+        if (n_trig > 48) eo.outline |= 2;
+        if (n_tr > 48 || (eo.team >= 2 && n_tr > 0)) eo.outline |= 4;
+    } else {
+        eo.outline = p->opts.outline < 0 ? 0 : p->opts.outline;
+    }
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
@@ -537,6 +554,25 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     return rc;
 }
 
+// Entry points select `device` for their CUDA calls and restore the caller's current
+// device on return (torch and other callers keep their own notion of it).
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != device) err = cudaSetDevice(device);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define DEVICE_GUARD(dev)                                                                                       \
+    DeviceGuard _guard(dev);                                                                                    \
+    if (_guard.err != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_guard.err))
+
 int check_range(vsb_plan* p, int64_t e0, int64_t e1) {
     if (!p) return fail(VSB_ERR_INVALID, "null plan");
     if (e0 < 0 || e1 < e0) return fail(VSB_ERR_INVALID, "invalid element range [" + std::to_string(e0) + ", " + std::to_string(e1) + ")");
@@ -749,7 +785,7 @@ int vsb_eval_device(vsb_plan* p, const void* in_buf, const int64_t* in_off, void
     if (e1 == e0) return VSB_OK;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
@@ -772,7 +808,7 @@ int vsb_eval_device_ptrs(vsb_plan* p, const void* const* ins_, void* const* outs
     if (e1 == e0) return VSB_OK;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     if ((n_in && !ins_) || (n_out && !outs_)) return fail(VSB_ERR_INVALID, "null pointer array");
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
@@ -798,7 +834,7 @@ int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const v
     if (steps < 0 || plane < e1) return fail(VSB_ERR_INVALID, "need steps >= 0 and plane >= e1");
     if (e1 == e0 || steps == 0) return VSB_OK;
     if (!ins_ || !outs_) return fail(VSB_ERR_INVALID, "null pointer array");
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
@@ -835,7 +871,7 @@ int vsb_eval_device_soa(vsb_plan* p, const void* const* ins_, void* const* outs_
     if (e1 == e0) return VSB_OK;
     if (ld < e1) return fail(VSB_ERR_INVALID, "ld must be >= e1");
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
@@ -855,7 +891,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     if (e1 == e0) return VSB_OK;
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     constexpr int kMaxPieces = 8;
     Variant* v;
     std::vector<cudaStream_t> streams;  // [0] H2D, [1] D2H, [2..] one compute stream per piece

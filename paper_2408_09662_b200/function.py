@@ -62,6 +62,35 @@ class Function:
                 raise ValueError(f"input {i}: batch/device differs from input 0")
         return batch, device
 
+    def _check_out(self, out, b, dev):
+        """Caller-provided outputs are written through raw pointers: check count, shape,
+        dtype, device and layout exactly (a mismatch would be an out-of-bounds write)."""
+        t = self.tape
+        out = list(out)
+        if len(out) != t.n_out:
+            raise ValueError(f"out: expected {t.n_out} tensors, got {len(out)}")
+        for j, o in enumerate(out):
+            if not isinstance(o, torch.Tensor):
+                raise TypeError(f"out {j}: expected a torch.Tensor, got {type(o).__name__}")
+            want = (b, t.nnz_out[j]) if self.layout == "aos" else (t.nnz_out[j], b)
+            if tuple(o.shape) != want:
+                raise ValueError(f"out {j}: expected shape {want}, got {tuple(o.shape)}")
+            if o.dtype != self.dtype:
+                raise ValueError(f"out {j}: dtype {o.dtype} != {self.dtype}")
+            if o.device != dev:
+                raise ValueError(f"out {j}: device {o.device} != {dev}")
+            if o.numel() == 0:
+                continue
+            if self.layout == "aos" and not o.is_contiguous():
+                raise ValueError(f"out {j}: an AoS output must be contiguous")
+            if self.layout == "soa" and o.shape[1] > 1 and o.stride(1) != 1:
+                raise ValueError(f"out {j}: an SoA output needs unit stride along the batch")
+        if self.layout == "soa":
+            lds = {o.stride(0) for o in out if o.shape[0] > 1 and o.numel()}
+            if len(lds) > 1:
+                raise ValueError(f"out: SoA outputs must share one leading dimension, got {sorted(lds)}")
+        return out
+
     def __call__(self, *inputs, out=None, batch: int | None = None, device=None):
         t = self.tape
         if t.n_in:
@@ -70,11 +99,15 @@ class Function:
             if batch is None:
                 raise ValueError("tape has no inputs: pass batch=")
             b, dev = int(batch), torch.device(device if device is not None else "cuda")
+            if dev.type == "cuda" and dev.index is None:
+                dev = torch.device("cuda", torch.cuda.current_device())
+        if out is not None:
+            out = self._check_out(out, b, dev)
         if self.layout == "aos":
             inputs = [x.contiguous() for x in inputs]
             outs = out if out is not None else [torch.empty((b, nz), dtype=self.dtype, device=dev) for nz in t.nnz_out]
         else:
-            inputs = [x if x.stride(1) == 1 else x.contiguous() for x in inputs]
+            inputs = [x if (x.shape[1] <= 1 or x.stride(1) == 1) else x.contiguous() for x in inputs]
             outs = out if out is not None else [torch.empty((nz, b), dtype=self.dtype, device=dev) for nz in t.nnz_out]
         if b == 0:
             return outs
@@ -83,11 +116,25 @@ class Function:
             self.plan.eval_device_ptrs([x.data_ptr() for x in inputs], [o.data_ptr() for o in outs], 0, b,
                                        dev.index or 0, stream)
         else:
-            lds = {x.stride(0) for x in inputs if x.shape[0] > 1} | {o.stride(0) for o in outs if o.shape[0] > 1}
-            ld = lds.pop() if len(lds) == 1 else None
-            if ld is None:
+            # one leading dimension for every row: the outputs' (caller-fixed) if given, else
+            # the inputs' common stride, else b; inputs off that stride are re-laid out
+            out_lds = {o.stride(0) for o in outs if o.shape[0] > 1}
+            in_lds = {x.stride(0) for x in inputs if x.shape[0] > 1}
+            if out is not None and out_lds:
+                ld = out_lds.pop()
+            elif len(in_lds) == 1 and (not out_lds or out_lds == in_lds):
+                ld = in_lds.pop()
+            else:
                 ld = b
-                inputs = [x.contiguous() for x in inputs]
-            self.plan.eval_device_soa([x.data_ptr() for x in inputs], [o.data_ptr() for o in outs], ld, 0, b,
+            if ld < b:
+                raise ValueError(f"SoA leading dimension {ld} < batch {b}")
+            fixed = []
+            for x in inputs:
+                if x.shape[0] > 1 and x.stride(0) != ld:
+                    y = torch.empty_strided(tuple(x.shape), (ld, 1), dtype=x.dtype, device=x.device)
+                    y.copy_(x)
+                    x = y
+                fixed.append(x)
+            self.plan.eval_device_soa([x.data_ptr() for x in fixed], [o.data_ptr() for o in outs], ld, 0, b,
                                       dev.index or 0, stream)
         return outs

@@ -1,0 +1,149 @@
+"""Acceptance criterion 1 of the reference on the GPU path.
+
+The reference checks ``batch_eval == serial_eval`` bit for bit on 100 fuzzer
+tapes of up to 1e4 instructions at B in {1, 7, 256, 4096}
+(/root/reference/pkg/tests/test_acceptance.py:69-111).  Here the same tape
+plan (tests/golden/make_acceptance_golden.py, run against the reference) is
+evaluated through the C ABI in every kernel regime this build has:
+
+* the default plan (thread mode; team mode above 4000 live ops),
+* forced team mode with the chunk splitter cutting the tape (cross-chunk
+  scratch, per-chunk re-loads of inputs),
+* forced 16-warp teams with a tiny shared-memory budget (cross-warp values
+  overflow to global scratch),
+* forced thread-mode chunking,
+
+and checked (1) against the reference's own outputs (golden rows),
+(2) against the pinned CPU oracle on all 4096 rows, (3) batch prefix rows
+and B=1 ``serial_eval`` calls bit for bit against the B=4096 run.
+
+``exact`` tapes (transcendental-free opcodes) must be bit-identical to the
+reference.  ``acc`` tapes (the reference fuzzer's full opcode set: tan, pow,
+atan2, exp, log on unbounded values, composed through kinks) are held to the
+fp64 contract ``|g - r| <= max(1e-12 max(|r|, 1), 4 * spread)``, where
+``spread`` is the reference algorithm's own drift under a 1-ulp change of its
+libm (``oracle.sensitivity``; zero wherever the value does not depend on a
+transcendental).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, assert_bitwise_or_nan, assert_parity
+from paper_2408_09662_b200 import BatchWorkspace, batch_eval, serial_eval
+from paper_2408_09662_b200.tape import deserialize
+
+SEED = {"acc": 5000, "exact": 6000}   # tests/golden/make_acceptance_golden.py
+ROWS = 64
+BATCHES = (1, 7, 256, 4096)
+
+
+def _golden():
+    return np.load(os.path.join(GOLDEN, "acceptance.npz"))
+
+
+def _tapes(z, fam):
+    n = len({k.split("__")[0] for k in z.files if k.startswith(fam) and k[len(fam)].isdigit()})
+    return [deserialize(bytes(z[f"{fam}{i}__tape"]).decode()) for i in range(n)]
+
+
+def inputs_for(fam, idx, nnz_in, batch):
+    rng = np.random.default_rng(SEED[fam] + idx)
+    return [rng.uniform(-2.0, 2.0, size=(batch, n)) for n in nnz_in]
+
+
+def stress_options(tape, idx):
+    """Plan options that force one of the non-default regimes (rotating by index)."""
+    n = tape.n_instructions
+    if n < 60:
+        return []
+    kind = idx % 3
+    if kind == 0:
+        return [{"team": 12, "chunk_ops": max(20, n // 3)}]
+    if kind == 1:
+        return [{"team": 16, "team_smem": 2048}]
+    return [{"team": 1, "chunk_ops": max(10, n // 4)}]
+
+
+@pytest.mark.parametrize("fam", ["acc", "exact"])
+def test_oracle_matches_reference_on_acceptance_tapes(fam):
+    """The oracle is bit-identical to the reference's batch_eval on every fuzz tape."""
+    z = _golden()
+    tapes = _tapes(z, fam)
+    assert len(tapes) == 100
+    sizes = [t.n_instructions for t in tapes]
+    assert min(sizes) >= 10 and max(sizes) <= 10_000 and max(sizes) > 4000   # test_acceptance.py:108-109
+    for idx, tape in enumerate(tapes):
+        ins = inputs_for(fam, idx, tape.nnz_in, ROWS)
+        outs = oracle.batch_eval(tape, ins, n_threads=2)
+        for j, o in enumerate(outs):
+            assert_bitwise_or_nan(o, z[f"{fam}{idx}__out{j}"], f"{fam}{idx} out {j}")
+
+
+def _gpu_eval(tape, ins, opts):
+    B = ins[0].shape[0] if ins else 1
+    ws = BatchWorkspace(tape, B)
+    for i, v in enumerate(ins):
+        ws.set_input(i, v)
+    batch_eval(tape, ws, plan_options=opts or None)
+    return [ws.output_matrix(j).copy() for j in range(tape.n_out)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam", ["exact", "acc"])
+def test_acceptance_fuzz_gpu(fam):
+    pytest.importorskip("torch")
+    from paper_2408_09662_b200 import Plan
+
+    z = _golden()
+    tapes = _tapes(z, fam)
+    engaged = {"team": 0, "team_chunked": 0, "overflow": 0, "thread_chunked": 0}
+    for idx, tape in enumerate(tapes):
+        master = inputs_for(fam, idx, tape.nnz_in, max(BATCHES))
+        if fam == "acc":
+            ref, spread = oracle.sensitivity(tape, master, n_threads=8)
+        else:
+            ref, spread = oracle.batch_eval(tape, master, n_threads=8), None
+
+        def check(got, what, rows=slice(None)):
+            for j, g in enumerate(got):
+                r = ref[j][rows]
+                if spread is None:
+                    assert_bitwise_or_nan(g, r, f"{what} out {j}")
+                else:
+                    assert_parity(g, r, spread[j][rows], what=f"{what} out {j}")
+
+        for opts in [{}] + stress_options(tape, idx):
+            what = f"{fam}{idx} ({tape.n_instructions} instr) {opts or 'default'}"
+            info = Plan(tape, **opts).info
+            if info["team"]:
+                engaged["team"] += 1
+                engaged["team_chunked"] += info["n_chunks"] > 1
+                engaged["overflow"] += info["overflow_slots"] > 0
+            elif info["n_chunks"] > 1:
+                engaged["thread_chunked"] += 1
+            full = _gpu_eval(tape, master, opts)
+            check(full, f"{what} B=4096")
+            # the reference's own outputs on the golden rows
+            for j, g in enumerate(full):
+                gold = z[f"{fam}{idx}__out{j}"]
+                if spread is None:
+                    assert_bitwise_or_nan(g[:ROWS], gold, f"{what} vs reference out {j}")
+                else:
+                    assert_parity(g[:ROWS], gold, spread[j][:ROWS], what=f"{what} vs reference out {j}")
+            # batch prefixes and single-instance calls are bit-identical to the B=4096 rows
+            for B in BATCHES[:-1]:
+                part = _gpu_eval(tape, [m[:B] for m in master], opts)
+                for j, (a, b) in enumerate(zip(part, full)):
+                    assert_bitwise_or_nan(a, b[:B], f"{what} B={B} vs B=4096 out {j}")
+            if not opts:
+                for e in (0, 4095):
+                    ser = serial_eval(tape, [m[e] for m in master])
+                    for j, (a, b) in enumerate(zip(ser, full)):
+                        assert_bitwise_or_nan(a, b[e], f"{what} serial_eval row {e} out {j}")
+    # every regime was exercised
+    assert engaged["team"] >= 20 and engaged["team_chunked"] >= 10, engaged
+    assert engaged["overflow"] >= 10 and engaged["thread_chunked"] >= 10, engaged

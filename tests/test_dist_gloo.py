@@ -1,8 +1,10 @@
-"""World-size-2 multi-process test of the batch-sharding plumbing on CPU
-(gloo).  Each rank evaluates its contiguous shard (with the CPU oracle as the
-per-rank evaluator, since this container has no GPU), the shards are
-gathered to rank 0 and must equal a single-process evaluation bit for bit;
-the timing reduction must return the max over ranks."""
+"""World-size-2 multi-process test of ``dist.batch_eval_ranks`` on CPU (gloo).
+
+Each rank evaluates its contiguous shard of one ``BatchWorkspace`` (the GPU
+call is replaced by the CPU oracle on the same [lo, hi) range, since this
+container has no GPU), the output shards are all-gathered, and every rank's
+workspace must then equal a single-process evaluation bit for bit; the timing
+reduction must return the max over ranks."""
 
 import os
 import socket
@@ -12,7 +14,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2408_09662_b200.dist import gather_rows, max_over_ranks, shard_bounds
+from paper_2408_09662_b200 import BatchWorkspace
+from paper_2408_09662_b200.dist import batch_eval_ranks, max_over_ranks, shard_bounds
 
 
 def _free_port():
@@ -36,12 +39,22 @@ def _worker(rank, world, port, batch, q):
     try:
         tape = workloads.load_tape("cartpole_rk4")
         ins = workloads.make_inputs("cartpole_rk4", batch, seed=42)
-        lo, hi = shard_bounds(batch, world, rank)
-        (out,) = oracle.batch_eval(tape, [v[lo:hi] for v in ins])
-        full = gather_rows(out, batch)
+        ws = BatchWorkspace(tape, batch)
+        for i, v in enumerate(ins):
+            ws.set_input(i, v)
+        seen = []
+
+        def shard(tape_, ws_, lo_, hi_):   # the per-rank evaluator: oracle on [lo, hi)
+            seen.append((lo_, hi_))
+            outs = oracle.batch_eval(tape_, [ws_.input_matrix(i)[lo_:hi_] for i in range(tape_.n_in)])
+            for j, o in enumerate(outs):
+                ws_.output_matrix(j)[lo_:hi_] = o
+
+        (full,) = batch_eval_ranks(tape, ws, evaluate=shard)
+        lo, hi = seen[0]
         t = max_over_ranks(float(rank + 1) * 1.5)
         dist.barrier()
-        q.put((rank, lo, hi, None if full is None else full.tobytes(), t))
+        q.put((rank, lo, hi, full.tobytes(), t))
     finally:
         dist.destroy_process_group()
 
@@ -76,6 +89,6 @@ def test_two_rank_shard_gather_and_max_timing():
     tape = workloads.load_tape("cartpole_rk4")
     ins = workloads.make_inputs("cartpole_rk4", batch, seed=42)
     (ref,) = oracle.batch_eval(tape, ins)
-    full = np.frombuffer(res[0][3], dtype=np.float64).reshape(ref.shape)
-    assert np.array_equal(full.view(np.uint64), ref.view(np.uint64))
-    assert res[1][3] is None
+    for r in res:   # every rank holds the whole batch after the final gather
+        full = np.frombuffer(r[3], dtype=np.float64).reshape(ref.shape)
+        assert np.array_equal(full.view(np.uint64), ref.view(np.uint64))
