@@ -50,6 +50,58 @@ WORKLOAD_CONFIG = {
 }
 
 
+def arm_config(args, world: int, tape) -> dict:
+    """The workload description both arms print (identical dicts: the driver compares them)."""
+    per_gpu = args.global_batch // max(world, 1) if args.global_batch else args.batch
+    total = args.global_batch if args.global_batch else args.batch * max(world, 1)
+    return {"workload": args.workload, "batch_per_gpu": per_gpu, "global_batch": total,
+            "description": WORKLOAD_CONFIG.get(args.workload, ""), "tape_rows": tape.n_instructions,
+            "parallelism": f"batch-sharded x{world} (no data-path collective)"}
+
+
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_numba(tape, inputs, threads: int, seconds: float = 3.0):
+    """The reference evaluator itself (numba ``run_range`` under ``vecsym.batchrt.batch_eval``,
+    batchrt.py:194-244, _kernels.py:54-206) from ``baseline/_ref`` on the host cores:
+    evals/s at W=1 and W=threads on bounded samples (2 warm-ups -- the first JITs --
+    then the median of >= 5 calls and >= `seconds` of work, the reference's bench.py:133-156
+    protocol).  None when the reference is not installed."""
+    if not os.path.isdir(os.path.join(REF_PATH, "vecsym")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/vsb_numba_cache")
+    if REF_PATH not in sys.path:
+        sys.path.append(REF_PATH)
+    try:
+        from vecsym.batchrt import BatchWorkspace as RefWorkspace
+        from vecsym.batchrt import batch_eval as ref_batch_eval
+        from vecsym.tape import deserialize as ref_deserialize
+
+        from paper_2408_09662_b200.tape import serialize
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"import: {e}"[:200]}
+    rtape = ref_deserialize(serialize(tape))
+    res = {"kind": "reference", "impl": "vecsym.batchrt.batch_eval (numba run_range), baseline/_ref",
+           "unit": "evals/s"}
+    for w in (1, threads):
+        B = max(w, min(inputs[0].shape[0], int(0.25 * w / max(tape.n_instructions * 4.5e-9, 1e-12))))
+        ws = RefWorkspace(rtape, B)
+        for i, v in enumerate(inputs):
+            ws.set_input(i, v[:B])
+        for _ in range(2):
+            ref_batch_eval(rtape, ws, n_threads=w)
+        rates, t_all = [], time.perf_counter()
+        while len(rates) < 5 or (time.perf_counter() - t_all < seconds and len(rates) < 100):
+            t0 = time.perf_counter()
+            ref_batch_eval(rtape, ws, n_threads=w)
+            rates.append(B / (time.perf_counter() - t0))
+        res[f"w{w}" if w == 1 else "w_all"] = statistics.median(rates)
+        res[f"sample_w{w}" if w == 1 else "sample_w_all"] = f"{B} instances x {len(rates)} calls"
+    res["cores"] = threads
+    return res
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -161,15 +213,17 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = Bs * args.steps / total
+    numba = reference_numba(tape, inputs, threads) if not args.no_numba else None
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "batch": args.batch, "description": WORKLOAD_CONFIG.get(args.workload, ""),
-                   "tape_rows": tape.n_instructions},
+        "higher_is_better": True, "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": arm_config(args, args.gpus, tape),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
                          "sample": f"{Bs} of {args.batch} instances per step, {args.steps} steps, "
-                                   "oracle/vs_oracle.c (C restatement of vecsym run_range/batch_eval), pthreads"},
+                                   "oracle/vs_oracle.c (C restatement of vecsym run_range/batch_eval), pthreads",
+                         "reference_numba": numba},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -302,12 +356,77 @@ def rollout_point(dev, B=10000, K=100, reps=5):
             "launches_per_rollout": r.launches_per_run}
 
 
+def batch_sweep(dev, local, hbm_gbs, steps=5):
+    """BASELINE metric's batch axis: evals/s of the headline tape and of the small
+    HBM-bound tape at B = 1e2 ... 1e6 (device-resident, L2 flushed per step)."""
+    import torch
+
+    import paper_2408_09662_b200 as vsb
+    import workloads
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    rows = []
+    for name, batches in (("srbm_mpc", (100, 1000, 4096, 10_000, 65_536, 100_000, 1_000_000)),
+                          ("cartpole_rk4", (100, 1000, 4096, 10_000, 65_536, 100_000, 1_000_000))):
+        tape = workloads.load_tape(name)
+        plan = vsb.get_plan(tape)
+        nin, nout = tape.nnz_in, tape.nnz_out
+        for B in batches:
+            ins = workloads.make_inputs(name, B, seed=4000)
+            in_off = np.concatenate([[0], np.cumsum(np.asarray(nin, dtype=np.int64) * B)])
+            out_off = np.concatenate([[0], np.cumsum(np.asarray(nout, dtype=np.int64) * B)])
+            d_in = torch.tensor(np.concatenate([v.ravel() for v in ins]), device=dev)
+            d_out = torch.empty(int(out_off[-1]), dtype=torch.float64, device=dev)
+
+            def step():
+                plan.eval_device(d_in.data_ptr(), in_off, d_out.data_ptr(), out_off, 0, B, local, stream.cuda_stream)
+
+            ms = []
+            for k in range(3 + steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                step()
+                b.record(stream)
+                b.synchronize()
+                if k >= 3:
+                    ms.append(a.elapsed_time(b))
+            t = statistics.median(ms) / 1e3
+            gbs = 8 * (sum(nin) + sum(nout)) * B / t / 1e9
+            rows.append({"workload": name, "batch": B, "value": B / t, "unit": "evals/s", "ms_per_step": t * 1e3,
+                         "hbm_frac": gbs / hbm_gbs})
+            del d_in, d_out
+    return rows
+
+
+def parity_all_rows(tape, inputs, got_flat, out_off, B):
+    """Every row of the timed batch against the CPU oracle (fp64 contract 1e-12 relative)."""
+    import oracle
+
+    ref = oracle.batch_eval(tape, inputs, n_threads=len(os.sched_getaffinity(0)))
+    worst, bad = 0.0, 0
+    for j, nz in enumerate(tape.nnz_out):
+        g = got_flat[out_off[j]:out_off[j + 1]].reshape(B, nz)
+        with np.errstate(invalid="ignore"):
+            err = np.abs(g - ref[j]) / np.maximum(np.abs(ref[j]), 1.0)
+        err[np.isnan(g) & np.isnan(ref[j])] = 0.0
+        if err.size:
+            worst = max(worst, float(np.nanmax(err)))
+            bad += int(np.count_nonzero(~(err <= 1e-12)))
+    bits = all(np.array_equal(got_flat[out_off[j]:out_off[j + 1]].reshape(B, nz).view(np.uint64),
+                              ref[j].view(np.uint64)) for j, nz in enumerate(tape.nnz_out))
+    return {"rows_checked": int(B), "max_rel_err": worst, "violations": bad, "bitwise_identical": bool(bits),
+            "tolerance": 1e-12, "ok": bad == 0}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2408_09662_b200 as vsb
     import workloads
+    from paper_2408_09662_b200.dist import batch_eval_ranks, max_over_ranks, shard_bounds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -318,8 +437,6 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     tape = workloads.load_tape(args.workload)
-    from paper_2408_09662_b200.dist import shard_bounds
-
     if args.global_batch:
         # strong scaling (config 4): one global batch split B*k//W over ranks
         lo, hi = shard_bounds(args.global_batch, world, rank)
@@ -330,15 +447,7 @@ def run_ours(args):
         total_instances = world * B
     inputs = workloads.make_inputs(args.workload, B, seed=1000 + rank)
     opts = {}
-    if args.block:
-        opts["block"] = args.block
-    if args.chunk_ops:
-        opts["chunk_ops"] = args.chunk_ops
-    if args.team:
-        opts["team"] = args.team
-    if args.min_blocks:
-        opts["min_blocks"] = args.min_blocks
-    for k in ("groups", "cluster", "outline", "phase_cost"):
+    for k in ("block", "chunk_ops", "team", "min_blocks", "groups", "cluster", "outline", "phase_cost"):
         if getattr(args, k):
             opts[k] = getattr(args, k)
     plan = vsb.get_plan(tape, **opts)
@@ -377,50 +486,43 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in evs]
-    total_ms = sum(step_ms)
-    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    total_ms = float(t_max.item())
+    total_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in evs), device=dev)
     clocks = sampler.stop() if sampler else None
 
-    # parity spot check of the timed configuration (oracle on a few rows)
-    parity = None
-    if rank == 0:
-        import oracle
+    # parity of the timed configuration: every row of this rank's batch vs the CPU oracle
+    parity = parity_all_rows(tape, inputs, d_out.cpu().numpy(), out_off, B) if rank == 0 else None
 
-        rows = np.random.default_rng(0).choice(B, size=min(B, 32), replace=False)
-        ref = oracle.batch_eval(tape, [v[rows] for v in inputs], n_threads=len(os.sched_getaffinity(0)))
-        out = d_out.cpu().numpy()
-        worst = 0.0
-        for j in range(tape.n_out):
-            g = out[out_off[j]:out_off[j + 1]].reshape(B, nout[j])[rows]
-            err = np.abs(g - ref[j]) / np.maximum(np.abs(ref[j]), 1.0)
-            worst = max(worst, float(np.nanmax(err)) if err.size else 0.0)
-        parity = {"rows_checked": int(rows.size), "max_rel_err": worst, "tolerance": 1e-12, "ok": worst <= 1e-12}
+    # end to end through the reference-shaped public API (pinned host buffers); strong
+    # scaling runs dist.batch_eval_ranks over one global workspace (shard, final gather)
+    if args.global_batch:
+        e2e_tape_ws = vsb.BatchWorkspace(tape, args.global_batch)
+        g_in = workloads.make_inputs(args.workload, args.global_batch, seed=1000) if world > 1 else inputs
+        for i, v in enumerate(g_in):
+            e2e_tape_ws.set_input(i, v)
 
-    # end-to-end through the reference-shaped public API (pinned host buffers)
-    ws = vsb.BatchWorkspace(tape, B)
-    for i, v in enumerate(inputs):
-        ws.set_input(i, v)
+        def e2e_call():
+            batch_eval_ranks(tape, e2e_tape_ws, device=local, plan_options=opts or None)
+    else:
+        e2e_tape_ws = vsb.BatchWorkspace(tape, B)
+        for i, v in enumerate(inputs):
+            e2e_tape_ws.set_input(i, v)
+
+        def e2e_call():
+            vsb.batch_eval(tape, e2e_tape_ws, device=local, plan_options=opts or None)
     # warm-up >= 1 s: the PCIe link of an idle B200 needs ~0.5 s of traffic before pinned H2D
     # reaches full speed (tools/h2d_probe2.py: 15-30 GB/s cold, 54 GB/s warm)
     t_warm = time.perf_counter()
     while time.perf_counter() - t_warm < 1.0:
-        vsb.batch_eval(tape, ws, device=local, plan_options=opts or None)
+        e2e_call()
     if world > 1:
         dist.barrier()
     e2e_steps = max(3, min(args.steps, 20))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        vsb.batch_eval(tape, ws, device=local, plan_options=opts or None)
-    e2e_s = time.perf_counter() - t0
-    t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        e2e_call()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device=dev)
     if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         dist.barrier()
-    e2e_s = float(t_e2e.item())
 
     if rank != 0:
         dist.destroy_process_group()
@@ -434,24 +536,26 @@ def run_ours(args):
     fp64_peak = 148 * 64 * sm_max_mhz * 1e6 / 1e12  # one non-fused DP op per lane per clock
     fp64_achieved = ops_eval * B / mean_s / 1e12
     value = total_instances * args.steps / (total_ms / 1e3)
+    e2e_value = total_instances * e2e_steps / e2e_s
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         Bs = cpu_sample_batch(tape, B, threads)
         rate, reps, secs = cpu_baseline(tape, [v[:Bs] for v in inputs], args.cpu_seconds, threads)
-        rate1 = None
-        if args.cpu_w1:
-            Bs1 = cpu_sample_batch(tape, B, 1)
-            rate1, _, _ = cpu_baseline(tape, [v[:Bs1] for v in inputs], 2.0, 1)
+        Bs1 = cpu_sample_batch(tape, B, 1)
+        rate1, _, _ = cpu_baseline(tape, [v[:Bs1] for v in inputs], 2.0, 1)
         cpu = {"value": rate, "unit": "evals/s", "cores": threads, "kind": "port",
                "sample": f"{Bs} instances x {reps} calls ({secs:.1f} s), W={threads} pthreads, "
                          "oracle/vs_oracle.c restating vecsym run_range/batch_eval",
-               "w1_value": rate1, "speedup_value_vs_cpu": value / rate, "speedup_e2e_vs_cpu":
-                   (world * B * e2e_steps / e2e_s) / rate}
+               "w1_value": rate1, "speedup_value_vs_cpu": value / rate, "speedup_e2e_vs_cpu": e2e_value / rate,
+               "reference_numba": None if args.no_numba else reference_numba(tape, inputs, threads)}
 
     ifetch = ifetch_roof(plan, info, B, mean_s, clocks)
-    secondary = secondary_points(dev, local, hbm_gbs) if (world == 1 and not args.no_secondary) else None
+    secondary = sweep = None
+    if world == 1 and not args.no_secondary:
+        secondary = secondary_points(dev, local, hbm_gbs)
+        sweep = batch_sweep(dev, local, hbm_gbs)
     traffic, traffic_src = committed_traffic(args.workload, info, B)
 
     line = {
@@ -459,14 +563,12 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "batch_per_gpu": B, "global_batch": total_instances,
-                   "description": WORKLOAD_CONFIG.get(args.workload, ""),
-                   "tape_rows": tape.n_instructions, "arith_ops_per_eval": ops_eval, "io_bytes_per_eval": bytes_eval,
-                   "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                   "parallelism": f"batch-sharded x{world} (no data-path collective)",
-                   "plan": {k: info[k] for k in ("n_chunks", "block", "scratch_slots", "scratch_loads",
-                                                 "scratch_stores", "max_regs", "max_local_bytes",
-                                                 "stage_in", "stage_out")}},
+        "config": arm_config(args, world, tape),
+        "workload_detail": {"arith_ops_per_eval": ops_eval, "io_bytes_per_eval": bytes_eval,
+                            "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                            "plan": {k: info[k] for k in ("team", "n_chunks", "block", "scratch_slots", "scratch_loads",
+                                                          "scratch_stores", "max_regs", "max_local_bytes",
+                                                          "phases", "est_efficiency", "code_bytes")}},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_gbs, "unit": "GB/s",
                      "frac": achieved_gbs / hbm_gbs, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
@@ -478,19 +580,71 @@ def run_ours(args):
                      "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "Tops/s",
                               "frac": fp64_achieved / fp64_peak,
                               "peak_def": "148 SM x 64 FP64 lanes x sm_max_mhz, 1 op/lane/clk (no FMA: --fmad=false)"}},
-        "e2e": {"value": total_instances * e2e_steps / e2e_s, "unit": "evals/s",
-                "h2d_bytes_per_step": 8 * sum(nin) * B, "d2h_bytes_per_step": 8 * sum(nout) * B,
-                "api": "paper_2408_09662_b200.batch_eval(tape, BatchWorkspace) [pinned host buffers]",
+        "e2e": {"value": e2e_value, "unit": "evals/s",
+                "h2d_bytes_per_step": 8 * sum(nin) * total_instances, "d2h_bytes_per_step": 8 * sum(nout) * total_instances,
+                "api": ("paper_2408_09662_b200.dist.batch_eval_ranks(tape, BatchWorkspace)" if args.global_batch else
+                        "paper_2408_09662_b200.batch_eval(tape, BatchWorkspace)") + " [pinned host buffers]",
                 "timing": f"{e2e_steps} synchronous calls, host wall clock, max over ranks"},
         "gpu_launches": args.steps * plan.launches_per_eval(B),
         "clocks": clocks,
         "parity": parity,
         "cpu_baseline": cpu,
         "secondary": secondary,
+        "batch_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_inprocess(args):
+    """One process driving N GPUs through the in-process sharder (``batch_eval(devices=...)``,
+    ``vsb_eval_host_sharded``: contiguous shards, a host thread + streams per GPU)."""
+    import torch
+
+    import paper_2408_09662_b200 as vsb
+    import workloads
+
+    n = min(args.gpus, torch.cuda.device_count())
+    tape = workloads.load_tape(args.workload)
+    total = args.global_batch or args.batch * n
+    ws = vsb.BatchWorkspace(tape, total)
+    for i, v in enumerate(workloads.make_inputs(args.workload, total, seed=1000)):
+        ws.set_input(i, v)
+    devs = list(range(n))
+    t_warm = time.perf_counter()
+    while time.perf_counter() - t_warm < 1.0:
+        vsb.batch_eval(tape, ws, devices=devs)
+    steps = max(3, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        vsb.batch_eval(tape, ws, devices=devs)
+    dt = time.perf_counter() - t0
+    nin, nout = tape.nnz_in, tape.nnz_out
+    print(json.dumps({"metric": METRIC, "value": total * steps / dt, "unit": "evals/s", "n_gpus": n,
+                      "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+                      "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": arm_config(args, n, tape),
+                      "e2e": {"value": total * steps / dt, "unit": "evals/s", "h2d_bytes_per_step": 8 * sum(nin) * total,
+                              "d2h_bytes_per_step": 8 * sum(nout) * total,
+                              "api": f"paper_2408_09662_b200.batch_eval(tape, BatchWorkspace, devices={devs})"}}),
+          flush=True)
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-launch this script with one process per GPU."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init lines name the rank count
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main():
@@ -516,10 +670,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the other-config points (cartpole/pendulum 1e6, humanoid/srbm 65536)")
+    ap.add_argument("--no-numba", action="store_true", help="skip timing the reference's numba evaluator")
+    ap.add_argument("--inprocess", action="store_true",
+                    help="N GPUs from one process via batch_eval(devices=range(N)) (e2e only)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.inprocess:
+        run_inprocess(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     else:
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         run_ours(args)
 
 

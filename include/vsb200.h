@@ -29,8 +29,8 @@
 extern "C" {
 #endif
 
-#define VSB_ABI_VERSION 3   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
-                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED */
+#define VSB_ABI_VERSION 4   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
+                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags */
 
 enum vsb_status {
     VSB_OK = 0,
@@ -67,11 +67,19 @@ typedef struct vsb_options {
                                warps over SMs (values cross SMs through DSMEM); 0 = auto   */
     int32_t outline;        /* ops emitted as shared __noinline__ subroutines (one copy in the
                                instruction cache instead of one per use): bit 0 DIV, bit 1
-                               SIN/COS; 0 = auto (team mode: both), -1 = none              */
+                               SIN/COS, bit 2 EXP/LOG/POW/TAN/ATAN2; 0 = auto (team mode:
+                               all; any plan: trig/others above 48 uses), -1 = none        */
     int32_t bulk_io;        /* thread mode, single kernel: persistent TMA (cp.async.bulk) tile
                                pipeline for the 128-instance tiles; 0 = auto (when every
                                resident CTA gets >= 3 tiles), 1 = whenever aligned, -1 = off */
+    int32_t flags;          /* VSB_FLAG_* code-generation variants (all off by default)     */
 } vsb_options;
+
+enum vsb_flags {
+    VSB_FLAG_PAIR_XFERS = 1,     /* team: two cross-warp values per 128-bit STS/LDS          */
+    VSB_FLAG_SPLIT_BARRIERS = 2, /* team: named-barrier arrive/sync instead of bar.sync     */
+    VSB_FLAG_DIV_RECIP = 4       /* fp64: divisions sharing a divisor use one reciprocal     */
+};
 
 typedef struct vsb_plan vsb_plan;
 

@@ -64,6 +64,7 @@ class Options(ctypes.Structure):
         ("cluster", ctypes.c_int32),
         ("outline", ctypes.c_int32),
         ("bulk_io", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 

@@ -299,7 +299,11 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     } else {
         eo.outline = p->opts.outline < 0 ? 0 : p->opts.outline;
     }
+    eo.pair_xfers = (p->opts.flags & VSB_FLAG_PAIR_XFERS) != 0;
+    eo.split_barriers = (p->opts.flags & VSB_FLAG_SPLIT_BARRIERS) != 0;
+    eo.div_recip = (p->opts.flags & VSB_FLAG_DIV_RECIP) != 0;
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
+    if (p->opts.flags) shape += "f" + std::to_string(p->opts.flags);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
     if (eo.outline) shape += "o" + std::to_string(eo.outline);
