@@ -30,7 +30,8 @@ extern "C" {
 #endif
 
 #define VSB_ABI_VERSION 4   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
-                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags */
+                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags,
+                               vsb_plan_prepare_rollout */
 
 enum vsb_status {
     VSB_OK = 0,
@@ -166,6 +167,11 @@ int vsb_eval_device_soa(vsb_plan *plan, const void *const *ins, void *const *out
 int vsb_rollout_device(vsb_plan *plan, int32_t state_in, int32_t state_out, const void *const *ins,
                        void *const *outs, int64_t plane, int64_t steps, int32_t record, int64_t e0,
                        int64_t e1, int32_t device, void *stream);
+
+/* Build (NVRTC-compile or load from the cubin cache) the closed-loop variant that
+ * vsb_rollout_device(plan, state_in, state_out, ...) launches, without a GPU.
+ * VSB_ERR_UNSUPPORTED when the plan has no single-kernel closed-loop form. */
+int vsb_plan_prepare_rollout(vsb_plan *plan, int32_t state_in, int32_t state_out);
 
 /* End-to-end over HOST memory (pinned or pageable), synchronous: H2D of the
  * inputs, the kernel chain, D2H of the outputs, pipelined in pieces over

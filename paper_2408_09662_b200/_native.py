@@ -21,7 +21,7 @@ VSB_F64, VSB_F32 = 0, 1
 EXPORTS = (
     "vsb_version", "vsb_last_error", "vsb_options_init", "vsb_plan_create", "vsb_plan_destroy",
     "vsb_plan_get_info", "vsb_plan_source", "vsb_plan_cubin", "vsb_plan_log", "vsb_eval_device", "vsb_eval_device_ptrs",
-    "vsb_eval_device_soa", "vsb_rollout_device",
+    "vsb_eval_device_soa", "vsb_rollout_device", "vsb_plan_prepare_rollout",
     "vsb_eval_host", "vsb_eval_host_sharded", "vsb_transpose", "vsb_launches_per_eval",
     "vsb_host_alloc", "vsb_host_free",
 )
@@ -141,6 +141,7 @@ def lib() -> ctypes.CDLL:
     L.vsb_eval_device_soa.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i64, i32, vp]
     L.vsb_rollout_device.argtypes = [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i64, i32, i64, i64, i32,
                                      vp]
+    L.vsb_plan_prepare_rollout.argtypes = [vp, i32, i32]
     L.vsb_eval_host.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i32]
     L.vsb_eval_host_sharded.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, ctypes.POINTER(i32), i32]
     L.vsb_transpose.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]

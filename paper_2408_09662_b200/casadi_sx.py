@@ -47,10 +47,96 @@ _DIRECT = {
     "OP_ATAN2": (OpCode.ATAN2, 2), "OP_FABS": (OpCode.FABS, 1), "OP_FMIN": (OpCode.FMIN, 2),
     "OP_FMAX": (OpCode.FMAX, 2),
 }
-# exact lowerings onto IR sequences
-_LOWERED = ("OP_TWICE", "OP_INV", "OP_IF_ELSE_ZERO")
+# exact lowerings onto IR sequences (comparisons and logic yield 1.0 / 0.0 like casadi's
+# casadi_math: x < y, x <= y, x == y, x != y, !x, x && y, x || y; NaN is truthy)
+_LOWERED = ("OP_TWICE", "OP_INV", "OP_IF_ELSE_ZERO", "OP_LT", "OP_LE", "OP_EQ", "OP_NE", "OP_NOT", "OP_AND",
+            "OP_OR")
 _PLUMBING = ("OP_CONST", "OP_INPUT", "OP_OUTPUT")
 SUPPORTED_OPS = tuple(_DIRECT) + _LOWERED + _PLUMBING
+
+
+def _lt(emit, o, x, y, t):
+    """o = (x < y) = STEP(y - x): y - x > 0 exactly when y > x for every IEEE pair (gradual
+    underflow keeps a nonzero difference nonzero, overflow keeps its sign; inf - inf and
+    NaN give NaN, and STEP(NaN) = 0 = (x < y))."""
+    emit(OpCode.SUB, t, y, x)
+    emit(OpCode.STEP, o, t)
+
+
+def _not(emit, o, x, t):
+    """o = !x = (x == 0): IF_ELSE(x, 0, 1) (NaN != 0 is truthy, as in C)."""
+    emit(OpCode.CONST, t, v=0.0)
+    emit(OpCode.CONST, t + 1, v=1.0)
+    emit(OpCode.IF_ELSE, o, x, t, t + 1)
+
+
+def _le(emit, o, x, y, t):
+    """o = (x <= y) = !(y < x) * ordered(x, y); ordered(v) = STEP(|v| + 1) (0 only for NaN).
+    inf <= inf: y < x is STEP(inf - inf) = 0, so the result is 1 as it must be."""
+    _lt(emit, t, y, x, t + 1)              # t = y < x
+    _not(emit, t, t, t + 1)                # t = !(y < x)
+    emit(OpCode.CONST, t + 1, v=1.0)
+    for v in (x, y):
+        emit(OpCode.FABS, t + 2, v)
+        emit(OpCode.ADD, t + 2, t + 2, t + 1)
+        emit(OpCode.STEP, t + 2, t + 2)    # 1 unless v is NaN
+        emit(OpCode.MUL, t, t, t + 2)
+    emit(OpCode.ASSIGN, o, t)
+
+
+def _lower_lt(emit, o, a, t):
+    _lt(emit, t, a[0], a[1], t + 1)
+    emit(OpCode.ASSIGN, o, t)
+    return 2
+
+
+def _lower_le(emit, o, a, t):
+    _le(emit, o, a[0], a[1], t)
+    return 3
+
+
+def _lower_eq(emit, o, a, t):
+    # x == y  <=>  x <= y and y <= x (both 0/1: the product is exact); NaN: 0
+    _le(emit, t + 3, a[0], a[1], t)
+    _le(emit, t + 4, a[1], a[0], t)
+    emit(OpCode.MUL, o, t + 3, t + 4)
+    return 5
+
+
+def _lower_ne(emit, o, a, t):
+    _lower_eq(emit, t + 5, a, t)
+    _not(emit, o, t + 5, t)
+    return 6
+
+
+def _lower_not(emit, o, a, t):
+    _not(emit, t + 2, a[0], t)
+    emit(OpCode.ASSIGN, o, t + 2)
+    return 3
+
+
+def _lower_and(emit, o, a, t):
+    # x && y: IF_ELSE(x, IF_ELSE(y, 1, 0), 0)
+    emit(OpCode.CONST, t, v=0.0)
+    emit(OpCode.CONST, t + 1, v=1.0)
+    emit(OpCode.IF_ELSE, t + 2, a[1], t + 1, t)
+    emit(OpCode.IF_ELSE, o, a[0], t + 2, t)
+    return 3
+
+
+def _lower_or(emit, o, a, t):
+    # x || y: IF_ELSE(x, 1, IF_ELSE(y, 1, 0))
+    emit(OpCode.CONST, t, v=0.0)
+    emit(OpCode.CONST, t + 1, v=1.0)
+    emit(OpCode.IF_ELSE, t + 2, a[1], t + 1, t)
+    emit(OpCode.IF_ELSE, o, a[0], t + 1, t + 2)
+    return 3
+
+
+# op name -> lowering(emit, out slot, operand slots, first scratch slot) -> scratch slots used;
+# every lowering reads its operands before it writes `out` (casadi may reuse an operand slot)
+_LOGIC = {"OP_LT": _lower_lt, "OP_LE": _lower_le, "OP_EQ": _lower_eq, "OP_NE": _lower_ne, "OP_NOT": _lower_not,
+          "OP_AND": _lower_and, "OP_OR": _lower_or}
 
 
 def _sparsity(sp) -> Sparsity:
@@ -112,6 +198,8 @@ def from_instructions(name: str, instructions: Iterable[Sequence], n_w: int, inp
                 extra = max(extra, 1)
                 emit(OpCode.CONST, zero, v=0.0)
                 emit(OpCode.IF_ELSE, outs[0], args[0], args[1], zero)
+            elif op_name in _LOGIC:
+                extra = max(extra, _LOGIC[op_name](emit, outs[0], args, scratch))
             else:
                 raise TapeError(f"instruction {k}: casadi operation {op_name} has no tape equivalent "
                                 f"(supported: {', '.join(SUPPORTED_OPS)})")

@@ -868,6 +868,20 @@ int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const v
     return VSB_OK;
 }
 
+int vsb_plan_prepare_rollout(vsb_plan* p, int32_t state_in, int32_t state_out) {
+    if (!p) return fail(VSB_ERR_INVALID, "null plan");
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if (state_in < 0 || state_in >= n_in || state_out < 0 || state_out >= n_out)
+        return fail(VSB_ERR_INVALID, "state input/output index out of range");
+    Variant* v;
+    std::lock_guard<std::mutex> lk(p->mu);
+    int rc = build_variant(p, kRollKey + state_in * 65536 + state_out, &v);
+    if (rc != VSB_OK) return rc;
+    if (!v->ks.chunks.front().roll || v->ks.chunks.size() != 1)
+        return fail(VSB_ERR_UNSUPPORTED, "no single-kernel closed-loop variant for this tape");
+    return VSB_OK;
+}
+
 int vsb_eval_device_soa(vsb_plan* p, const void* const* ins_, void* const* outs_, int64_t ld, int64_t e0, int64_t e1,
                         int32_t device, void* stream) {
     int rc = check_range(p, e0, e1);

@@ -153,6 +153,11 @@ class Plan:
                                                int(steps), int(bool(record)), int(e0), int(e1), int(device),
                                                ctypes.c_void_p(stream)))
 
+    def prepare_rollout(self, state_in: int = 0, state_out: int = 0) -> None:
+        """Compile the closed-loop variant ``rollout_device`` launches (no GPU needed);
+        raises ``_native.UnsupportedError`` when the plan has none."""
+        check(_native.lib().vsb_plan_prepare_rollout(self._h, int(state_in), int(state_out)))
+
     def eval_host(self, in_ptr, in_off, out_ptr, out_off, e0, e1, device=0):
         in_off = np.ascontiguousarray(in_off, dtype=np.int64)
         out_off = np.ascontiguousarray(out_off, dtype=np.int64)

@@ -180,3 +180,34 @@ def test_casadi_tape_on_gpu():
     vsb.batch_eval(tape, ws)
     for j, e in enumerate(expected(x, y)):
         assert_close(ws.output_matrix(j), e)
+
+
+_SPECIAL = np.array([0.0, -0.0, 1.0, -1.0, 2.5, -2.5, 1e-310, -1e-310, 5e-324, 1e308, -1e308, np.inf, -np.inf, np.nan])
+_CMP = {
+    "OP_LT": lambda x, y: x < y, "OP_LE": lambda x, y: x <= y, "OP_EQ": lambda x, y: x == y,
+    "OP_NE": lambda x, y: x != y, "OP_AND": lambda x, y: (x != 0) & (y != 0), "OP_OR": lambda x, y: (x != 0) | (y != 0),
+    "OP_NOT": lambda x, y: x == 0,
+}
+
+
+@pytest.mark.parametrize("op", sorted(_CMP))
+@pytest.mark.parametrize("alias", [False, True])
+def test_comparison_and_logic_lowerings_exact(op, alias):
+    """casadi's comparison / logic ops (1.0 or 0.0, NaN truthy, IEEE ordering incl. signed zeros,
+    infinities, subnormals and NaN) lowered onto STEP / IF_ELSE / FABS / arithmetic rows:
+    checked against numpy's comparisons on every pair of special values (CPU oracle).
+    ``alias``: the result overwrites an operand's work slot, as casadi's register reuse does."""
+    import oracle
+
+    x = np.repeat(_SPECIAL, _SPECIAL.size)[:, None]
+    y = np.tile(_SPECIAL, _SPECIAL.size)[:, None]
+    out = 0 if alias else 2
+    args = [0] if op == "OP_NOT" else [0, 1]
+    instr = [("OP_INPUT", [0], [0, 0], 0.0), ("OP_INPUT", [1], [1, 0], 0.0), (op, [out], args, 0.0),
+             ("OP_OUTPUT", [0, 0], [out], 0.0)]
+    tape = from_instructions("cmp", instr, 3, [1, 1], [1])
+    (got,) = oracle.batch_eval(tape, [x, y])
+    want = _CMP[op](x, y).astype(np.float64)
+    bad = np.flatnonzero(got[:, 0] != want[:, 0])
+    assert bad.size == 0, [(x[i, 0], y[i, 0], got[i, 0], want[i, 0]) for i in bad[:5]]
+    assert not np.signbit(got).any()
