@@ -311,8 +311,11 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     if (roll) shape += "r" + std::to_string(eo.roll_in) + "_" + std::to_string(eo.roll_out);
     v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
 
-    std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
-                                      "-Xptxas=-v"};
+    // -lineinfo embeds the whole PTX text in the cubin (2-3x its size; the in-tree cache
+    // travels to the GPU box), so it is on only for profiling runs: VSB_LINEINFO=1
+    std::vector<std::string> nopts = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-Xptxas=-v"};
+    static const bool lineinfo = getenv("VSB_LINEINFO") && atoi(getenv("VSB_LINEINFO")) != 0;
+    if (lineinfo) nopts.push_back("-lineinfo");
     if (p->opts.maxrregcount > 0) nopts.push_back("-maxrregcount=" + std::to_string(p->opts.maxrregcount));
     const size_t C = v->ks.chunks.size();
     v->compiled.resize(C);
