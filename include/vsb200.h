@@ -30,7 +30,7 @@ extern "C" {
 #endif
 
 #define VSB_ABI_VERSION 4   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
-                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags,
+                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags/tma_stages,
                                vsb_plan_prepare_rollout */
 
 enum vsb_status {
@@ -74,6 +74,7 @@ typedef struct vsb_options {
                                pipeline for the 128-instance tiles; 0 = auto (when every
                                resident CTA gets >= 3 tiles), 1 = whenever aligned, -1 = off */
     int32_t flags;          /* VSB_FLAG_* code-generation variants (all off by default)     */
+    int32_t tma_stages;     /* tile buffers of the persistent TMA pipeline; 0 = auto (2)    */
 } vsb_options;
 
 enum vsb_flags {

@@ -65,6 +65,7 @@ class Options(ctypes.Structure):
         ("outline", ctypes.c_int32),
         ("bulk_io", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("tma_stages", ctypes.c_int32),
     ]
 
 

@@ -229,10 +229,19 @@ std::string literal(double v, bool f32) {
 }
 
 const char* kPrelude = R"(// generated by paper_2408_09662_b200 (vsb200) -- do not edit
+// Team kernels: every warp runs its own switch case, so the warps of a CTA reach DIFFERENT
+// barrier instructions.  bar.sync is barrier.sync.aligned, which PTX defines only when every
+// thread of the CTA executes the same instruction (compute-sanitizer synccheck flags it:
+// profiles/r2_sanitizer.md); the non-aligned barrier.sync / barrier.arrive are the legal form.
+#ifndef VS_BAR_ALIGNED
+#define VS_BAR() asm volatile("barrier.sync 0;" ::: "memory")
+#define VS_BSYNC(id) asm volatile("barrier.sync %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
+#define VS_BARV(id) asm volatile("barrier.arrive %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
+#else
 #define VS_BAR() asm volatile("bar.sync 0;" ::: "memory")
-// named barriers: sync = arrive + wait (acquire), arrive = release without waiting
 #define VS_BSYNC(id) asm volatile("bar.sync %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 #define VS_BARV(id) asm volatile("bar.arrive %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
+#endif
 template <int NNZ, int OFF, int STRIDE>
 __device__ __forceinline__ void vs_stage_in(real* __restrict__ sm, const real* __restrict__ g, int cnt) {
     // coalesced 16-byte loads of a contiguous [rows, NNZ] tile -> padded smem rows
@@ -545,6 +554,12 @@ private:
     void emit_roll_kernel(Chunk& ch, Out& b) const;
     void emit_thread_chunk(int c, Chunk& ch, Out& b);
     void emit_tma_kernel(Chunk& ch, Out& b) const;
+    // tile buffers of the persistent TMA pipeline (loads in flight = stages - 1 while one computes)
+    int tma_stages() const {
+        static const int env = getenv("VSB_TMA_STAGES") ? atoi(getenv("VSB_TMA_STAGES")) : 0;
+        const int s = env > 0 ? env : opt.tma_stages;
+        return s < 2 ? 2 : (s > 8 ? 8 : s);
+    }
     void emit_team_chunk(int c, Chunk& ch, Out& b);
     void team_barrier_plan(TeamPlan& tp, const Chunk& ch);
     void team_cross_warp_values(TeamPlan& tp, Chunk& ch, int c);
@@ -700,6 +715,9 @@ void Emitter::build_header() {
     TWl = team ? opt.team / TK : 0;               // warp streams per CTA
     ks.groups = TG;
     ks.cluster = TK;
+    // A/B knob: VSB_BAR_ALIGNED=1 emits the (formally undefined here) aligned bar.sync
+    static const bool bar_aligned = getenv("VSB_BAR_ALIGNED") && atoi(getenv("VSB_BAR_ALIGNED")) != 0;
+    if (bar_aligned) hdr.s += "#define VS_BAR_ALIGNED 1\n";
     hdr.put("#define VS_BS %d\n", team ? TWl * TG * 32 : opt.block);
     hdr.put("#define VS_IPB %d\n", team ? 32 * TG : opt.block);   // instances per CTA (team: per cluster)
     hdr.s += "#define VS_NSLOT @@NSLOT@@LL\n";                   // scratch rows per instance (patched below)
@@ -1088,20 +1106,21 @@ void Emitter::emit_thread_chunk(int c, Chunk& ch, Out& b) {
     // buffers with cp.async.bulk (one bulk copy per input / output array, completion on
     // an mbarrier), the next tiles' loads in flight while the current tile computes
     const bool tma = opt.bulk_io && same_kernel && !soa && ni_tot > 0 && no_tot > 0 &&
-                     2 * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
+                     tma_stages() * (ni_tot + no_tot) * opt.block * rsz + 64 <= 200 * 1024;
     if (tma) emit_tma_kernel(ch, b);
     if (roll_possible()) emit_roll_kernel(ch, b);
 }
 
 void Emitter::emit_tma_kernel(Chunk& ch, Out& b) const {
     ch.tma = true;
+    const int NS = tma_stages();
     const int64_t IT = ni_tot * opt.block, OT = no_tot * opt.block;  // tile sizes (elements)
-    ch.tma_smem_bytes = 2 * (IT + OT) * rsz + 16;
+    ch.tma_smem_bytes = NS * (IT + OT) * rsz + 8 * NS;
     b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s_tma(const VsArgs A) {\n", opt.min_blocks, ch.name.c_str());
     b.put("    extern __shared__ __align__(128) real vs_smem[];\n");
-    b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", 2 * (IT + OT));
+    b.put("    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(vs_smem + %" PRId64 ");\n", NS * (IT + OT));
     b.put("    const long long ntiles = A.n / VS_BS;   // full tiles; the partial tail is done after the loop\n");
-    b.put("    if (threadIdx.x == 0) { vs_mbar_init(mbar, 1); vs_mbar_init(mbar + 1, 1); VS_FENCE_MBAR_INIT(); }\n");
+    b.put("    if (threadIdx.x == 0) { for (int s = 0; s < %d; ++s) vs_mbar_init(mbar + s, 1); VS_FENCE_MBAR_INIT(); }\n", NS);
     b.put("    __syncthreads();\n");
     // loads of one tile into buffer bs
     Out ld;
@@ -1117,17 +1136,18 @@ void Emitter::emit_tma_kernel(Chunk& ch, Out& b) const {
     ld.put("    };\n");
     b.s += ld.s;
     b.put("    long long tile = blockIdx.x;\n");
-    b.put("    if (threadIdx.x == 0) {\n");
-    b.put("        if (tile < ntiles) issue(tile, 0);\n");
-    b.put("        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);\n");
-    b.put("    }\n");
+    b.put("    if (threadIdx.x == 0)\n");
+    b.put("        for (int s = 0; s < %d; ++s)\n", NS);
+    b.put("            if (tile + s * (long long)gridDim.x < ntiles) issue(tile + s * (long long)gridDim.x, s);\n");
     b.put("    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {\n");
-    b.put("        const int bs = k & 1;\n");
-    b.put("        vs_mbar_wait(mbar + bs, (k >> 1) & 1);\n");
-    b.put("        if (threadIdx.x == 0 && k >= 2) VS_BULK_WAIT_READ1();  // out buffer bs free again\n");
+    b.put("        const int bs = k %% %d;\n", NS);
+    b.put("        vs_mbar_wait(mbar + bs, (k / %d) & 1);\n", NS);
+    // the out buffer bs was last handed to a bulk store NS tiles ago: at most NS-1 groups may
+    // still be reading
+    b.put("        if (threadIdx.x == 0 && k >= %d) asm volatile(\"cp.async.bulk.wait_group.read %d;\" ::: \"memory\");\n", NS, NS - 1);
     b.put("        __syncthreads();\n");
     b.put("        const real* ib = vs_smem + bs * %" PRId64 ";\n", IT);
-    b.put("        real* ob = vs_smem + %" PRId64 " + bs * %" PRId64 ";\n", 2 * IT, OT);
+    b.put("        real* ob = vs_smem + %" PRId64 " + bs * %" PRId64 ";\n", NS * IT, OT);
     for (int i = 0; i < n_in; ++i)
         b.put("        const real* __restrict__ I%d = ib + %" PRId64 " + threadIdx.x * %" PRId64 ";\n", i,
               p.in_base[i] * opt.block, p.nnz_in[i]);
@@ -1148,7 +1168,7 @@ void Emitter::emit_tma_kernel(Chunk& ch, Out& b) const {
               p.nnz_out[j], p.out_base[j] * opt.block, p.nnz_out[j] * opt.block * rsz);
     }
     b.put("            VS_BULK_COMMIT();\n");
-    b.put("            if (tile + 2 * (long long)gridDim.x < ntiles) issue(tile + 2 * (long long)gridDim.x, bs);\n");
+    b.put("            if (tile + %d * (long long)gridDim.x < ntiles) issue(tile + %d * (long long)gridDim.x, bs);\n", NS, NS);
     b.put("        }\n");
     b.put("    }\n");
     // the partial last tile (< 128 instances): one CTA, direct global loads/stores;

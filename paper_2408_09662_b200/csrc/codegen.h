@@ -94,6 +94,7 @@ struct EmitOptions {
     bool pair_xfers = false;   // team mode: 128-bit paired cross-warp exchange (STS.128 / LDS.128)
     bool split_barriers = false;  // team mode: named-barrier arrive/sync instead of a CTA barrier per phase
     bool bulk_io = true;       // thread mode, single kernel: also emit a persistent TMA (cp.async.bulk) variant
+    int tma_stages = 2;        // tile buffers of that pipeline (VSB_TMA_STAGES overrides)
     // thread mode, single kernel: also emit `<name>_roll`, a K-step closed-loop kernel feeding
     // output `roll_out` back into input `roll_in` in registers (-1: none)
     int roll_in = -1, roll_out = -1;

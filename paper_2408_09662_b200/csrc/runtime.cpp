@@ -20,6 +20,7 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <fcntl.h>
 #include <sys/stat.h>
 #include <thread>
 #include <unistd.h>
@@ -171,6 +172,8 @@ int compile_one(const vsb::Chunk& ch, const std::vector<std::string>& opts, cons
     const std::string path = cache_dir.empty() ? "" : cache_dir + "/" + key + ".cubin";
     if (!path.empty() && read_file(path, &out->cubin)) {
         out->cache_hit = true;
+        utimensat(AT_FDCWD, path.c_str(), nullptr, 0);   // mark as used (build() prunes stale entries)
+        utimensat(AT_FDCWD, (path + ".log").c_str(), nullptr, 0);
         std::vector<char> log;
         if (read_file(path + ".log", &log)) out->log.assign(log.begin(), log.end());
         parse_ptxas(out->log, out);
@@ -304,6 +307,8 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.div_recip = (p->opts.flags & VSB_FLAG_DIV_RECIP) != 0;
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
     if (p->opts.flags) shape += "f" + std::to_string(p->opts.flags);
+    eo.tma_stages = p->opts.tma_stages > 0 ? p->opts.tma_stages : 2;
+    if (eo.tma_stages != 2) shape += "s" + std::to_string(eo.tma_stages);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
     if (eo.outline) shape += "o" + std::to_string(eo.outline);
@@ -913,7 +918,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
     if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
     DEVICE_GUARD(device);
-    constexpr int kMaxPieces = 8;
+    constexpr int kMaxPieces = 8, kMaxSplit = 4;
     Variant* v;
     std::vector<cudaStream_t> streams;  // [0] H2D, [1] D2H, [2..] one compute stream per piece
     {
@@ -922,7 +927,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
         if (rc != VSB_OK) return rc;
         auto& ss = p->streams[device];
-        while (ss.size() < 2 + kMaxPieces) {
+        while (ss.size() < 2 + kMaxPieces + 2 * (kMaxSplit - 1)) {
             cudaStream_t s;
             CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
             ss.push_back(s);
@@ -1007,9 +1012,40 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     };
     const bool one_in = pieces == 1 && n_in > 0 && contiguous(in_off, p->prog.nnz_in);
     const bool one_out = pieces == 1 && n_out > 0 && contiguous(out_off, p->prog.nnz_out);
+    // one contiguous copy each way, optionally split over several streams (copy engines):
+    // VSB_COPY_SPLIT=k (default 1)
+    static const int copy_split = std::max(1, std::min(kMaxSplit, getenv("VSB_COPY_SPLIT") ? atoi(getenv("VSB_COPY_SPLIT")) : 1));
+    while (ws->events.size() < static_cast<size_t>(2 * pieces + 1 + 4 * kMaxSplit)) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ws->events.push_back(e);
+    }
+    auto split_copy = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t main,
+                          int stream0, int ev0) -> cudaError_t {
+        const int k = bytes >= (size_t(1) << 20) ? copy_split : 1;
+        const size_t part = (bytes / k + 255) / 256 * 256;
+        cudaError_t err = cudaSuccess;
+        for (int q = 0; q < k && err == cudaSuccess; ++q) {
+            const size_t lo = q * part, len = std::min(bytes, lo + part) - std::min(bytes, lo);
+            if (!len) continue;
+            cudaStream_t st = q == 0 ? main : streams[stream0 + q - 1];
+            if (q) {   // start after everything `main` already has queued
+                cudaEventRecord(ws->events[ev0 + q], main);
+                cudaStreamWaitEvent(st, ws->events[ev0 + q], 0);
+            }
+            err = cudaMemcpyAsync(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len, kind, st);
+            if (q) {
+                cudaEventRecord(ws->events[ev0 + kMaxSplit + q], st);
+                cudaStreamWaitEvent(main, ws->events[ev0 + kMaxSplit + q], 0);
+            }
+        }
+        return err;
+    };
+    const int ev_split = static_cast<int>(2 * pieces + 1);
     if (one_in && p->prog.in_base[n_in] > 0) {
-        cudaError_t e = cudaMemcpyAsync(wb + off_in[0], hin + (in_off[0] + e0 * p->prog.nnz_in[0]) * rs,
-                                        static_cast<size_t>(n * p->prog.in_base[n_in] * rs), cudaMemcpyHostToDevice, sh);
+        cudaError_t e = split_copy(wb + off_in[0], hin + (in_off[0] + e0 * p->prog.nnz_in[0]) * rs,
+                                   static_cast<size_t>(n * p->prog.in_base[n_in] * rs), cudaMemcpyHostToDevice, sh,
+                                   2 + kMaxPieces, ev_split);
         if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
         cudaEventRecord(ev[0], sh);
     }
@@ -1041,8 +1077,9 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     }
     if (one_out && rc == VSB_OK && p->prog.out_base[n_out] > 0) {
         cudaStreamWaitEvent(sd, ev[pieces], 0);
-        cudaError_t e = cudaMemcpyAsync(hout + (out_off[0] + e0 * p->prog.nnz_out[0]) * rs, wb + off_out[0],
-                                        static_cast<size_t>(n * p->prog.out_base[n_out] * rs), cudaMemcpyDeviceToHost, sd);
+        cudaError_t e = split_copy(hout + (out_off[0] + e0 * p->prog.nnz_out[0]) * rs, wb + off_out[0],
+                                   static_cast<size_t>(n * p->prog.out_base[n_out] * rs), cudaMemcpyDeviceToHost, sd,
+                                   2 + kMaxPieces + (kMaxSplit - 1), ev_split + 2 * kMaxSplit);
         if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
     }
     // 3. D2H in piece order

@@ -30,7 +30,10 @@ def jobs() -> list[tuple]:
         out.append(("workload", name, {"team": 1}))
         out += [("workload", name, o) for _, o in VARIANTS]
     out += [("workload", name, {"dtype": "float32"}) for name in sorted(FP32_RTOL)]
-    out += [("workload", "srbm_mpc", {"team": 8}), ("workload", "pendulum", {"bulk_io": 1})]
+    out += [("workload", "srbm_mpc", {"team": 8})]
+    for name in ("pendulum", "cartpole_rk4", "example"):
+        out += [("workload", name, o) for o in ({"bulk_io": 1}, {"bulk_io": -1}, {"bulk_io": 1, "tma_stages": 3},
+                                                 {"bulk_io": 1, "tma_stages": 4})]
     return out
 
 

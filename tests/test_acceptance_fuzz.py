@@ -51,8 +51,14 @@ def _tapes(z, fam):
 
 
 def inputs_for(fam, idx, nnz_in, batch):
+    """Rows [0, ROWS) are exactly the golden's inputs (make_acceptance_golden.inputs_for);
+    further rows come from a second seeded stream."""
     rng = np.random.default_rng(SEED[fam] + idx)
-    return [rng.uniform(-2.0, 2.0, size=(batch, n)) for n in nnz_in]
+    head = [rng.uniform(-2.0, 2.0, size=(min(batch, ROWS), n)) for n in nnz_in]
+    if batch <= ROWS:
+        return head
+    rng2 = np.random.default_rng(SEED[fam] + idx + 1_000_000)
+    return [np.concatenate([h, rng2.uniform(-2.0, 2.0, size=(batch - ROWS, n))]) for h, n in zip(head, nnz_in)]
 
 
 def stress_options(tape, idx):

@@ -412,6 +412,10 @@ def test_tma_tile_pipeline_equals_classic_kernel(name, B):
     assert vsb.get_plan(tape, bulk_io=1).info["n_chunks"] == 1
     for a, b in zip(fast, plain):
         assert_bitwise_or_nan(a.cpu().numpy(), b.cpu().numpy(), f"{name} B={B}")
+    for stages in (3, 4):                           # deeper tile pipelines
+        deep = vsb.Function(tape, bulk_io=1, tma_stages=stages)(*xs)
+        for a, b in zip(deep, plain):
+            assert_bitwise_or_nan(a.cpu().numpy(), b.cpu().numpy(), f"{name} B={B} stages={stages}")
     if B <= 4103:
         ref = oracle.batch_eval(tape, ins)
         for a, r in zip(fast, ref):
