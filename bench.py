@@ -592,9 +592,9 @@ def run_ours(args):
         "secondary": secondary,
         "batch_sweep": sweep,
     }
-    print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        dist.destroy_process_group()   # before printing: NCCL's INFO lines must not follow the JSON line
+    print(json.dumps(line), flush=True)
 
 
 def run_inprocess(args):

@@ -30,7 +30,7 @@ extern "C" {
 #endif
 
 #define VSB_ABI_VERSION 4   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
-                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags/tma_stages,
+                               3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags/tma_stages/lockstep,
                                vsb_plan_prepare_rollout */
 
 enum vsb_status {
@@ -75,6 +75,9 @@ typedef struct vsb_options {
                                resident CTA gets >= 3 tiles), 1 = whenever aligned, -1 = off */
     int32_t flags;          /* VSB_FLAG_* code-generation variants (all off by default)     */
     int32_t tma_stages;     /* tile buffers of the persistent TMA pipeline; 0 = auto (2)    */
+    int32_t lockstep;       /* team mode: independent team CTAs per thread-block cluster that
+                               meet at a relaxed cluster barrier every 8 phases (instruction-
+                               cache sharing within a GPC); 0/1 = off, <= 8                 */
 } vsb_options;
 
 enum vsb_flags {

@@ -66,6 +66,7 @@ class Options(ctypes.Structure):
         ("bulk_io", ctypes.c_int32),
         ("flags", ctypes.c_int32),
         ("tma_stages", ctypes.c_int32),
+        ("lockstep", ctypes.c_int32),
     ]
 
 

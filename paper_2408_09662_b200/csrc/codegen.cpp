@@ -715,6 +715,7 @@ void Emitter::build_header() {
     TWl = team ? opt.team / TK : 0;               // warp streams per CTA
     ks.groups = TG;
     ks.cluster = TK;
+    ks.lockstep = (team && TK == 1 && opt.lockstep > 1) ? opt.lockstep : 1;   // grid: whole clusters
     // A/B knob: VSB_BAR_ALIGNED=1 emits the (formally undefined here) aligned bar.sync
     static const bool bar_aligned = getenv("VSB_BAR_ALIGNED") && atoi(getenv("VSB_BAR_ALIGNED")) != 0;
     if (bar_aligned) hdr.s += "#define VS_BAR_ALIGNED 1\n";
@@ -1571,9 +1572,11 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     max_overflow = std::max(max_overflow, n_glob);
     ch.smem_bytes = n_smem * IPB * rsz;
 
-    if (K > 1)
-        b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", K,
-              opt.min_blocks, nbuf);
+    const int LS = (K == 1 && opt.lockstep > 1) ? opt.lockstep : 1;
+    const int LE = std::max(1, opt.lockstep_every);
+    if (K > 1 || LS > 1)
+        b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n",
+              K > 1 ? K : LS, opt.min_blocks, nbuf);
     else
         b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
     b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
@@ -1684,7 +1687,14 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
             } else if (ph + 1 < P) {
                 b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
             }
+            // lockstep: every LE phases wait for the previous relaxed cluster arrival, arrive again
+            // (the CTAs of a cluster drift at most LE phases apart); a last wait before exit
+            if (LS > 1 && !split && (ph + 1) % LE == 0 && ph + 1 < P) {
+                if (ph + 1 > LE) b.put("%sasm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n", ind);
+                b.put("%sasm volatile(\"barrier.cluster.arrive.relaxed;\" ::: \"memory\");\n", ind);
+            }
         }
+        if (LS > 1 && !split && P > LE) b.put("%sasm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n", ind);
         b.put("        break;\n    }\n");
     }
     b.put("    }\n}\n");

@@ -83,6 +83,10 @@ struct EmitOptions {
     // consumer CTA's shared memory (DSMEM) and phases end in a cluster barrier.
     int groups = 1;
     int cluster = 1;
+    // lockstep L > 1 (team mode, cluster == 1): L independent team CTAs per thread-block cluster
+    // (one GPC) meet at a relaxed cluster barrier every `lockstep_every` phases, so that their
+    // identical instruction streams stay close enough to share the GPC's instruction-cache fills
+    int lockstep = 1, lockstep_every = 8;
     // bit 0: DIV, bit 1: SIN/COS emitted as calls to shared __noinline__
     // subroutines (straight-line team code is instruction-fetch bound; one
     // resident copy of the division / trig sequence beats one per use)
@@ -126,8 +130,8 @@ struct Kernelset {
     std::vector<Chunk> chunks;
     int64_t scratch_slots = 0;     // SoA scratch rows needed per instance
     int block = 128;
-    int team = 0, groups = 1, cluster = 1;
-    bool cluster_dims_one() const { return cluster == 1 && groups == 1; }
+    int team = 0, groups = 1, cluster = 1, lockstep = 1;
+    bool cluster_dims_one() const { return cluster == 1 && groups == 1 && lockstep == 1; }
     int64_t live_total = 0;        // team mode: max over chunks of the summed per-warp live peaks
     bool f32 = false;
     Layout layout = Layout::AOS;

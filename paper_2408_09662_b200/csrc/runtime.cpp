@@ -308,6 +308,14 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     std::string shape = eo.team >= 2 ? "t" + std::to_string(eo.team) : "b" + std::to_string(eo.block);
     if (p->opts.flags) shape += "f" + std::to_string(p->opts.flags);
     eo.tma_stages = p->opts.tma_stages > 0 ? p->opts.tma_stages : 2;
+    {
+        static const int env_ls = getenv("VSB_LOCKSTEP") ? atoi(getenv("VSB_LOCKSTEP")) : 0;
+        static const int env_le = getenv("VSB_LOCKSTEP_EVERY") ? atoi(getenv("VSB_LOCKSTEP_EVERY")) : 0;
+        eo.lockstep = std::max(1, std::min(8, env_ls > 0 ? env_ls : p->opts.lockstep));
+        eo.lockstep_every = env_le > 0 ? env_le : 8;
+        if (eo.team >= 2 && eo.cluster == 1 && eo.lockstep > 1)
+            shape += "l" + std::to_string(eo.lockstep) + "e" + std::to_string(eo.lockstep_every);
+    }
     if (eo.tma_stages != 2) shape += "s" + std::to_string(eo.tma_stages);
     if (eo.team >= 2 && (eo.groups > 1 || eo.cluster > 1))
         shape += "g" + std::to_string(eo.groups) + "k" + std::to_string(eo.cluster);
@@ -466,7 +474,8 @@ int64_t pick_ipc(const vsb::Kernelset& ks, int64_t m, int n_sm) {
 int64_t units_for(const vsb::Kernelset& ks, int64_t m, int n_sm) {
     if (m <= 0) return 0;
     const int64_t c = pick_ipc(ks, m, n_sm);
-    const int64_t u = (m + c - 1) / c;
+    int64_t u = (m + c - 1) / c;
+    if (ks.lockstep > 1) u = (u + ks.lockstep - 1) / ks.lockstep * ks.lockstep;   // whole clusters
     static const bool fill = getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) != 0;
     if (ks.team >= 2 && !fill && ks.cluster_dims_one() && u < 24) return 24;
     return u;

@@ -40,13 +40,13 @@ class Plan:
     chained kernel; -1 never splits), ``min_blocks``, ``maxrregcount``,
     ``smem_budget``, ``wave``, ``compile_threads``, ``verbose``, ``cache_dir``, ``team``,
     ``groups``, ``cluster``, ``outline``, ``bulk_io``, ``flags`` (``VSB_FLAG_*``: 1 paired
-    cross-warp exchange, 2 split barriers, 4 shared-reciprocal division), ``tma_stages``.
+    cross-warp exchange, 2 split barriers, 4 shared-reciprocal division), ``tma_stages``, ``lockstep``.
     """
 
     def __init__(self, tape, *, dtype="float64", block=0, chunk_ops=0, min_blocks=0, maxrregcount=0,
                  smem_budget=0, wave=0, compile_threads=0, verbose=False, cache_dir=None, team=0,
                  phase_cost=0, priority=0, libdevice_trig=False, team_smem=0, groups=0, cluster=0, outline=0, bulk_io=0, flags=0,
-                 tma_stages=0):
+                 tma_stages=0, lockstep=0):
         self.tape: InstructionTape = as_tape(tape)
         self.dtype_code = _dtype_code(dtype)
         self.np_dtype = np.float32 if self.dtype_code == _native.VSB_F32 else np.float64
@@ -73,6 +73,7 @@ class Plan:
         opts.bulk_io = int(bulk_io)
         opts.flags = int(flags)
         opts.tma_stages = int(tma_stages)
+        opts.lockstep = int(lockstep)
         self._cache_dir = None if cache_dir is None else str(cache_dir).encode()
         opts.cache_dir = self._cache_dir
         code, values = self.tape.packed()

@@ -12,7 +12,8 @@ tolerances per config, and every off-by-default code-generation variant.
   unicycle_mpc -- the penalty-SQP solves amplify fp32 rounding) and set with ~3-7x headroom; the reference is
   fp64-only, so these are this build's own contract.
 * variants: thread-block clusters, instance groups, paired 128-bit exchange,
-  split barriers and shared-reciprocal division must not change a bit.
+  split barriers, shared-reciprocal division and lockstep clusters must not
+  change a bit.
 """
 
 import numpy as np
@@ -90,6 +91,7 @@ VARIANTS = [
     ("pair+split", {"team": 12, "flags": 3}),
     ("divrecip_team", {"team": 8, "flags": 4}),
     ("divrecip_thread", {"team": 1, "flags": 4}),
+    ("lockstep4", {"team": 8, "lockstep": 4}),
 ]
 
 

@@ -537,3 +537,21 @@ def test_function_out_argument_is_validated():
     assert torch.equal(os_.t(), o)
     with pytest.raises(ValueError):
         fs(*sins, out=[torch.empty((64, 4), dtype=torch.float64, device="cuda")])
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_sharder_over_distinct_devices():
+    # vsb_eval_host_sharded over real devices [0, 1, ...]: contiguous B*k//W shards
+    # (batchrt.py:189-191), one host thread + stream set per GPU, no collective
+    n = min(torch.cuda.device_count(), 8)
+    tape = workloads.load_tape("srbm_mpc")
+    B = 1000 + n * 37
+    ins = workloads.make_inputs("srbm_mpc", B, seed=88)
+    ws = BatchWorkspace(tape, B)
+    for i, v in enumerate(ins):
+        ws.set_input(i, v)
+    batch_eval(tape, ws, devices=list(range(n)))
+    ref = oracle.batch_eval(tape, ins, n_threads=8)
+    for j, r in enumerate(ref):
+        assert_close(ws.output_matrix(j), r, RTOL64, f"sharded over {n} GPUs out {j}")
+    assert torch.cuda.current_device() == 0   # the device guard restored the caller's device
