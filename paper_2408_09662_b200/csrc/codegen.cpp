@@ -233,12 +233,16 @@ const char* kPrelude = R"(// generated by paper_2408_09662_b200 (vsb200) -- do n
 // barrier instructions.  bar.sync is barrier.sync.aligned, which PTX defines only when every
 // thread of the CTA executes the same instruction (compute-sanitizer synccheck flags it:
 // profiles/r2_sanitizer.md); the non-aligned barrier.sync / barrier.arrive are the legal form.
-#ifndef VS_BAR_ALIGNED
+#if !defined(VS_BAR_ALIGNED)
 #define VS_BAR() asm volatile("barrier.sync 0;" ::: "memory")
 #define VS_BSYNC(id) asm volatile("barrier.sync %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 #define VS_BARV(id) asm volatile("barrier.arrive %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 #else
+#if VS_BAR_ALIGNED == 2
+#define VS_BAR() asm volatile("bar.sync 15, %0;" :: "n"(VS_BS) : "memory")
+#else
 #define VS_BAR() asm volatile("bar.sync 0;" ::: "memory")
+#endif
 #define VS_BSYNC(id) asm volatile("bar.sync %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 #define VS_BARV(id) asm volatile("bar.arrive %0, %1;" :: "n"(id), "n"(VS_BS) : "memory")
 #endif
@@ -717,8 +721,8 @@ void Emitter::build_header() {
     ks.cluster = TK;
     ks.lockstep = (team && TK == 1 && opt.lockstep > 1) ? opt.lockstep : 1;   // grid: whole clusters
     // A/B knob: VSB_BAR_ALIGNED=1 emits the (formally undefined here) aligned bar.sync
-    static const bool bar_aligned = getenv("VSB_BAR_ALIGNED") && atoi(getenv("VSB_BAR_ALIGNED")) != 0;
-    if (bar_aligned) hdr.s += "#define VS_BAR_ALIGNED 1\n";
+    static const int bar_aligned = getenv("VSB_BAR_ALIGNED") ? atoi(getenv("VSB_BAR_ALIGNED")) : 0;
+    if (bar_aligned) hdr.put("#define VS_BAR_ALIGNED %d\n", bar_aligned);
     hdr.put("#define VS_BS %d\n", team ? TWl * TG * 32 : opt.block);
     hdr.put("#define VS_IPB %d\n", team ? 32 * TG : opt.block);   // instances per CTA (team: per cluster)
     hdr.s += "#define VS_NSLOT @@NSLOT@@LL\n";                   // scratch rows per instance (patched below)

@@ -67,7 +67,8 @@ def assert_close(got, ref, rtol=RTOL64, what=""):
 def assert_parity(got, ref, spread=None, rtol=RTOL64, what="", factor=4.0):
     """The fp64 parity contract: |g - r| <= max(rtol * max(|r|, 1), factor * spread)
     where ``spread`` is the reference algorithm's own deviation when its
-    transcendental results move by one ulp (oracle.sensitivity; zero for
+    transcendental results move by the ulps two conforming libms may differ by
+    (oracle.sensitivity: 1 for sin/cos, 2 for exp/log, 3 for pow/tan/atan2; zero for
     transcendental-free tapes, which therefore must match to 1e-12 -- and are
     in fact bit-identical).  NaN == NaN, infinities exact."""
     got = np.asarray(got, dtype=np.float64)

@@ -17,31 +17,44 @@ import io
 import subprocess
 import sys
 
+# (label, metric, wanted unit) -- values are converted from the unit row of the raw page
 ROWS = [
-    ("duration (us)", "gpu__time_duration.sum", 1e-3),
-    ("DRAM read (MB)", "dram__bytes_read.sum", 1e-6),
-    ("DRAM write (MB)", "dram__bytes_write.sum", 1e-6),
-    ("DRAM throughput (% peak)", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
-    ("SM throughput (% peak)", "sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
-    ("issue slots busy (%)", "sm__inst_issued.avg.pct_of_peak_sustained_active", 1),
-    ("executed IPC (active)", "sm__inst_executed.avg.per_cycle_active", 1),
-    ("instructions executed (M warp-instr)", "smsp__inst_executed.sum", 1e-6),
-    ("achieved occupancy (%)", "sm__warps_active.avg.pct_of_peak_sustained_active", 1),
-    ("registers / thread", "launch__registers_per_thread", 1),
-    ("grid size", "launch__grid_size", 1),
-    ("block size", "launch__block_size", 1),
-    ("dynamic smem / block (KB)", "launch__shared_mem_per_block_dynamic", 1e-3),
-    ("local load sectors (M)", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", 1e-6),
-    ("local store sectors (M)", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", 1e-6),
-    ("smem ld bank conflicts (M)", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", 1e-6),
-    ("smem st bank conflicts (M)", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", 1e-6),
-    ("L2 hit rate (%)", "lts__t_sector_hit_rate.pct", 1),
-    ("FP64 pipe (% peak)", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
-    ("FP64 instr executed (M)", "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", 1e-6 / 32),
+    ("duration (us)", "gpu__time_duration.sum", "us"),
+    ("DRAM read (MB)", "dram__bytes_read.sum", "MB"),
+    ("DRAM write (MB)", "dram__bytes_write.sum", "MB"),
+    ("DRAM throughput (% peak)", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", ""),
+    ("SM throughput (% peak)", "sm__throughput.avg.pct_of_peak_sustained_elapsed", ""),
+    ("issue slots busy (%)", "sm__inst_issued.avg.pct_of_peak_sustained_active", ""),
+    ("executed IPC (active)", "sm__inst_executed.avg.per_cycle_active", ""),
+    ("instructions executed (M warp-instr)", "smsp__inst_executed.sum", "M"),
+    ("achieved occupancy (%)", "sm__warps_active.avg.pct_of_peak_sustained_active", ""),
+    ("registers / thread", "launch__registers_per_thread", ""),
+    ("grid size", "launch__grid_size", ""),
+    ("block size", "launch__block_size", ""),
+    ("dynamic smem / block (KB)", "launch__shared_mem_per_block_dynamic", "KB"),
+    ("local load sectors (M)", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "M"),
+    ("local store sectors (M)", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", "M"),
+    ("global load sectors (M)", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "M"),
+    ("global load requests (M)", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "M"),
+    ("smem ld bank conflicts (M)", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "M"),
+    ("smem st bank conflicts (M)", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "M"),
+    ("L2 hit rate (%)", "lts__t_sector_hit_rate.pct", ""),
+    ("FP64 pipe (% peak)", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", ""),
 ]
-STALL_PREFIX = "smsp__average_warp_latency_issue_stalled_"
-STALL_SUFFIX = ".ratio"
-MIX_PREFIX = "sass__inst_executed_per_opcode"
+STALL_PREFIX = "smsp__average_warps_issue_stalled_"
+STALL_SUFFIX = "_per_issue_active.ratio"
+_SCALE = {  # unit row -> factor to the base (bytes, seconds, count)
+    "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3, "byte/block": 1,
+    "ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
+}
+_WANT = {"us": 1e-6, "MB": 1e6, "KB": 1e3, "M": 1e6}
+
+
+def convert(value: float, unit: str, want: str) -> float:
+    if not want:
+        return value
+    base = value * _SCALE.get(unit.strip(), 1.0)
+    return base / _WANT[want]
 
 
 def raw_rows(path):
@@ -59,18 +72,18 @@ def main():
         for row in data:
             name = row[idx.get("Kernel Name", 0)][:48]
             vals = {}
-            for label, metric, scale in ROWS:
+            for label, metric, want in ROWS:
                 i = idx.get(metric)
                 if i is None or not row[i].strip():
                     vals[label] = "-"
                     continue
                 try:
-                    vals[label] = f"{float(row[i].replace(',', '')) * scale:.4g}"
+                    vals[label] = f"{convert(float(row[i].replace(',', '')), units[i], want):.4g}"
                 except ValueError:
                     vals[label] = row[i]
             stalls = []
             for h, i in idx.items():
-                if h.startswith(STALL_PREFIX) and h.endswith(STALL_SUFFIX) and "not_issued" not in h:
+                if h.startswith(STALL_PREFIX) and h.endswith(STALL_SUFFIX):
                     try:
                         stalls.append((float(row[i].replace(',', '')), h[len(STALL_PREFIX):-len(STALL_SUFFIX)]))
                     except ValueError:
