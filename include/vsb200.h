@@ -75,9 +75,9 @@ typedef struct vsb_options {
                                resident CTA gets >= 3 tiles), 1 = whenever aligned, -1 = off */
     int32_t flags;          /* VSB_FLAG_* code-generation variants (all off by default)     */
     int32_t tma_stages;     /* tile buffers of the persistent TMA pipeline; 0 = auto (2)    */
-    int32_t lockstep;       /* team mode: independent team CTAs per thread-block cluster that
-                               meet at a relaxed cluster barrier every 8 phases (instruction-
-                               cache sharing within a GPC); 0/1 = off, <= 8                 */
+    int32_t lockstep;       /* team mode: CTAs per thread-block cluster for multi-wave launches;
+                               the CTAs meet at a relaxed cluster barrier every 4 phases and
+                               keep sharing instruction-cache fills; 0 = auto (2), 1 = off */
 } vsb_options;
 
 enum vsb_flags {

@@ -541,6 +541,9 @@ private:
     bool stage_in = false, stage_out = false, same_kernel = false;
     int TK = 1, TG = 1, TWl = 0;
     Out hdr;
+    // team mode, rematerialised reloads: current version of a value's name in the warp being
+    // emitted (0 = "v<u>", k = "v<u>_<k>")
+    std::vector<int32_t> ver_;
 
     void cut_chunks();
     void plan_cross_chunk();
@@ -794,6 +797,7 @@ void Emitter::build_header() {
 std::string Emitter::opnd(int32_t u) const {
     const Node& nu = p.nodes[u];
     if (nu.op == OP_CONST) return literal(nu.imm, f32);
+    if (!ver_.empty() && ver_[u] > 0) return "v" + std::to_string(u) + "_" + std::to_string(ver_[u]);
     return "v" + std::to_string(u);
 }
 
@@ -1535,10 +1539,32 @@ void Emitter::team_live_stats(TeamPlan& tp, int c) {
             std::vector<int64_t> delta(pos + 2, 0);
             for (int64_t q = 0; q < N; ++q)
                 if (first[q] >= 0) { delta[first[q]] += 1; delta[lastu[q] + 1] -= 1; }
-            int64_t run = 0, peak = 0;
-            for (int64_t i = 0; i <= pos; ++i) { run += delta[i]; peak = std::max(peak, run); }
+            int64_t run = 0, peak = 0, at = 0;
+            for (int64_t i = 0; i <= pos; ++i) {
+                run += delta[i];
+                if (run > peak) { peak = run; at = i; }
+            }
             worst = std::max(worst, peak);
             sum_peak += peak;
+            static const int dbg = getenv("VSB_LIVE_STATS") ? atoi(getenv("VSB_LIVE_STATS")) : 0;
+            if (dbg >= 2) {
+                // what the peak is made of: inputs, imports from earlier chunks, other warps' values,
+                // own values; and how many of those are idle for > 64 of this warp's ops at the peak
+                int64_t n_in = 0, n_imp = 0, n_x = 0, n_own = 0, idle = 0;
+                for (int64_t q = 0; q < N; ++q) {
+                    if (first[q] < 0 || first[q] > at || lastu[q] < at) continue;
+                    const Node& nq = p.nodes[q];
+                    const bool inch = tp.warp_of[q] >= 0;
+                    if (nq.op == OP_INPUT) ++n_in;
+                    else if (!inch) ++n_imp;
+                    else if (tp.warp_of[q] != w) ++n_x;
+                    else ++n_own;
+                }
+                (void)idle;
+                fprintf(stderr, "  chunk %d warp %d: peak %lld at op %lld/%lld = inputs %lld, chunk imports %lld, "
+                        "cross-warp %lld, own %lld\n", c, w, (long long)peak, (long long)at, (long long)pos,
+                        (long long)n_in, (long long)n_imp, (long long)n_x, (long long)n_own);
+            }
         }
         if (getenv("VSB_LIVE_STATS"))
             fprintf(stderr, "chunk %d W=%d: per-warp live doubles peak max %lld mean %.0f\n", c, W, (long long)worst,
@@ -1578,9 +1604,12 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
 
     const int LS = (K == 1 && opt.lockstep > 1) ? opt.lockstep : 1;
     const int LE = std::max(1, opt.lockstep_every);
-    if (K > 1 || LS > 1)
+    // lockstep kernels carry no compile-time cluster shape: the runtime launches them as
+    // clusters of LS CTAs when the grid spans several waves and plainly (implicit 1-CTA
+    // clusters, where the cluster barrier is a CTA barrier) otherwise
+    if (K > 1)
         b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n",
-              K > 1 ? K : LS, opt.min_blocks, nbuf);
+              K, opt.min_blocks, nbuf);
     else
         b.put("extern \"C\" __global__ void __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n", opt.min_blocks, nbuf);
     b.put("    extern __shared__ __align__(16) real vs_smem[];\n");
@@ -1618,13 +1647,37 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     }
     b.put("    switch (warp) {\n");
     std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
+    // rematerialisation (VSB_REMAT_GAP=g > 0): an input or a value imported from an earlier
+    // chunk that this warp last touched more than g of its ops ago is loaded again (from the
+    // input row / the chunk scratch, both read-only in this kernel) instead of being held in a
+    // register across the gap -- fewer registers live, fewer ptxas spills
+    static const int remat_gap = getenv("VSB_REMAT_GAP") ? atoi(getenv("VSB_REMAT_GAP")) : 0;
+    std::vector<int64_t> lastpos(N, 0);
+    ver_.assign(N, 0);
+    int64_t pos = 0, remat_id = 0;
     for (int w = 0; w < W; ++w) {
         b.put("    case %d: {\n", w);
         const char* ind = "        ";
         auto ensure = [&](int32_t u) {
             const Node& nu = p.nodes[u];
-            if (nu.op == OP_CONST || have[u] == w) return;
+            if (nu.op == OP_CONST) return;
+            const bool remat_ok = remat_gap > 0 && !f32 && !soa && (nu.op == OP_INPUT || !in_chunk(u));
+            if (have[u] == w) {
+                if (!remat_ok || pos - lastpos[u] <= remat_gap) return;
+                // reload under a fresh name; the asm text is unique so that no pass merges it
+                // with the earlier load (and not volatile, so ptxas may schedule it early)
+                const int k = ++ver_[u];
+                if (nu.op == OP_INPUT)
+                    b.put("%sreal v%d_%d; asm(\"ld.global.nc.f64 %%0, [%%1]; // r%lld\" : \"=d\"(v%d_%d) : \"l\"(I%d + %d));\n",
+                          ind, u, k, (long long)++remat_id, u, k, nu.in_i, nu.in_k);
+                else
+                    b.put("%sreal v%d_%d; asm(\"ld.global.f64 %%0, [%%1]; // r%lld\" : \"=d\"(v%d_%d) : \"l\"(S + %d * VS_IPB));\n",
+                          ind, u, k, (long long)++remat_id, u, k, slot_of[u]);
+                ++ch.loads;
+                return;
+            }
             have[u] = w;
+            ver_[u] = 0;
             if (nu.op == OP_INPUT) { input_load(b, u, ind); return; }
             if (!in_chunk(u)) {  // imported from an earlier chunk
                 b.put("%sconst real v%d = S[%d * VS_IPB];\n", ind, u, slot_of[u]);
@@ -1652,7 +1705,9 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
             for (int32_t q : ts.seq[w][ph]) {
                 const Node& nd = p.nodes[q];
                 if (sync_at[q] >= 0) b.put("%sVS_BSYNC(%d);\n", ind, 1 + sync_at[q] % 15);
+                ++pos;
                 for (int k = 0; k < kArity[nd.op]; ++k) ensure(nd.arg[k]);
+                for (int k = 0; k < kArity[nd.op]; ++k) lastpos[nd.arg[k]] = pos;
                 if (partner[q] >= 0 && warp_of[partner[q]] != w) {
                     // mate lives on another warp: no pairing
                     b.put("%sconst real v%d = %s;\n", ind, q, expr_of(nd).c_str());
@@ -1702,6 +1757,7 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
         b.put("        break;\n    }\n");
     }
     b.put("    }\n}\n");
+    ver_.clear();
 }
 
 Kernelset Emitter::run() {

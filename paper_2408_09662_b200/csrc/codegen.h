@@ -131,7 +131,7 @@ struct Kernelset {
     int64_t scratch_slots = 0;     // SoA scratch rows needed per instance
     int block = 128;
     int team = 0, groups = 1, cluster = 1, lockstep = 1;
-    bool cluster_dims_one() const { return cluster == 1 && groups == 1 && lockstep == 1; }
+    bool cluster_dims_one() const { return cluster == 1 && groups == 1; }
     int64_t live_total = 0;        // team mode: max over chunks of the summed per-warp live peaks
     bool f32 = false;
     Layout layout = Layout::AOS;

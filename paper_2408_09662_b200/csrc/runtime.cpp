@@ -311,8 +311,11 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     {
         static const int env_ls = getenv("VSB_LOCKSTEP") ? atoi(getenv("VSB_LOCKSTEP")) : 0;
         static const int env_le = getenv("VSB_LOCKSTEP_EVERY") ? atoi(getenv("VSB_LOCKSTEP_EVERY")) : 0;
-        eo.lockstep = std::max(1, std::min(8, env_ls > 0 ? env_ls : p->opts.lockstep));
-        eo.lockstep_every = env_le > 0 ? env_le : 8;
+        // auto (0): pairs, every 4 phases, for team plans (measured: humanoid_rbd B=65536
+        // 0.94 -> 0.71 ms, srbm_mpc 6.29 -> 5.98 ms; one-wave batches launch unclustered)
+        const int want = env_ls > 0 ? env_ls : (p->opts.lockstep == 0 ? 2 : p->opts.lockstep);
+        eo.lockstep = std::max(1, std::min(8, want));
+        eo.lockstep_every = env_le > 0 ? env_le : 4;
         if (eo.team >= 2 && eo.cluster == 1 && eo.lockstep > 1)
             shape += "l" + std::to_string(eo.lockstep) + "e" + std::to_string(eo.lockstep_every);
     }
@@ -475,7 +478,8 @@ int64_t units_for(const vsb::Kernelset& ks, int64_t m, int n_sm) {
     if (m <= 0) return 0;
     const int64_t c = pick_ipc(ks, m, n_sm);
     int64_t u = (m + c - 1) / c;
-    if (ks.lockstep > 1) u = (u + ks.lockstep - 1) / ks.lockstep * ks.lockstep;   // whole clusters
+    // lockstep kernels launched as clusters (several waves of CTAs): whole clusters
+    if (ks.lockstep > 1 && u > n_sm) u = (u + ks.lockstep - 1) / ks.lockstep * ks.lockstep;
     static const bool fill = getenv("VSB_IPC_FILL") && atoi(getenv("VSB_IPC_FILL")) != 0;
     if (ks.team >= 2 && !fill && ks.cluster_dims_one() && u < 24) return 24;
     return u;
@@ -563,8 +567,28 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
         for (size_t c = 0; c < v->kerns.size(); ++c) {
             const auto& ch = v->ks.chunks[c];
             const int64_t grid = units_for(v->ks, m, n_sm) * ch.cluster;
-            cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
-                                             dim3(ch.threads), args, static_cast<size_t>(ch.smem_bytes), stream);
+            cudaError_t e;
+            if (v->ks.lockstep > 1 && grid > n_sm) {
+                // several waves: pairs (lockstep) of CTAs share a cluster and meet at a relaxed
+                // cluster barrier every few phases -- their identical instruction streams stay
+                // together (humanoid_rbd B=65536: 0.94 -> 0.71 ms, profiles/r2_summary.md)
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(static_cast<unsigned>(grid));
+                cfg.blockDim = dim3(ch.threads);
+                cfg.dynamicSmemBytes = static_cast<size_t>(ch.smem_bytes);
+                cfg.stream = stream;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = static_cast<unsigned>(v->ks.lockstep);
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(v->kerns[c]), args);
+            } else {
+                e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
+                                     dim3(ch.threads), args, static_cast<size_t>(ch.smem_bytes), stream);
+            }
             if (e != cudaSuccess) {
                 rc = fail(VSB_ERR_CUDA, std::string("cudaLaunchKernel(") + v->ks.chunks[c].name + "): " + cudaGetErrorString(e));
                 break;

@@ -110,7 +110,10 @@ def test_acceptance_fuzz_gpu(fam):
     for idx, tape in enumerate(tapes):
         master = inputs_for(fam, idx, tape.nnz_in, max(BATCHES))
         if fam == "acc":
-            ref, spread = oracle.sensitivity(tape, master, n_threads=8)
+            # 10 direction patterns: kinked random tapes (tan of a 1e20 argument fed through
+            # FMIN/IF_ELSE, e.g. acc33) have outputs that jump between branches under a few-ulp
+            # libm change; 3 patterns can all land on one branch
+            ref, spread = oracle.sensitivity(tape, master, seeds=tuple(range(1, 11)), n_threads=8)
         else:
             ref, spread = oracle.batch_eval(tape, master, n_threads=8), None
 
