@@ -29,9 +29,9 @@
 extern "C" {
 #endif
 
-#define VSB_ABI_VERSION 4   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
+#define VSB_ABI_VERSION 5   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
                                3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags/tma_stages/lockstep,
-                               vsb_plan_prepare_rollout */
+                               vsb_plan_prepare_rollout; 5: vsb_plan_info.n_cse */
 
 enum vsb_status {
     VSB_OK = 0,
@@ -113,6 +113,8 @@ typedef struct vsb_plan_info {
     int32_t cluster;         /* CTAs per cluster (team mode)                             */
     int64_t remote_stores;   /* per-warp DSMEM stores to other CTAs, summed over chunks  */
     int64_t code_bytes;      /* SASS bytes (.text.*) of all chunks; /16 = instructions    */
+    int64_t n_cse;           /* arithmetic rows answered by an existing value (exact value
+                                numbering + the x*1, x/1, x-(+0), x+(-0), x*(-1), -(-x) identities) */
 } vsb_plan_info;
 
 const char *vsb_version(void);
@@ -135,6 +137,11 @@ int vsb_plan_source(vsb_plan *plan, int32_t chunk, const char **source);
 int vsb_plan_cubin(vsb_plan *plan, int32_t chunk, const void **data, int64_t *size);
 /* Compiler log of the last compile (may be empty). */
 int vsb_plan_log(vsb_plan *plan, const char **log);
+/* Diagnostics: copy `bytes` of the __device__ variable `name` of chained kernel `chunk`'s module
+ * (AoS variant) on `device` to `host` -- e.g. the per-phase clock64() trace the team kernels
+ * record when compiled with VSB_PHASE_TRACE=1 (`vs_ptrace`, tools/phase_trace.py). */
+int vsb_debug_read_global(vsb_plan *plan, int32_t chunk, const char *name, int32_t device, void *host,
+                          int64_t bytes);
 
 /* run_range over DEVICE memory: elements [e0, e1) of an env-major workspace
  * (in_buf/out_buf device pointers, in_off/out_off HOST arrays of n_in+1 /

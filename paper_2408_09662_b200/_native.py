@@ -23,7 +23,7 @@ EXPORTS = (
     "vsb_plan_get_info", "vsb_plan_source", "vsb_plan_cubin", "vsb_plan_log", "vsb_eval_device", "vsb_eval_device_ptrs",
     "vsb_eval_device_soa", "vsb_rollout_device", "vsb_plan_prepare_rollout",
     "vsb_eval_host", "vsb_eval_host_sharded", "vsb_transpose", "vsb_launches_per_eval",
-    "vsb_host_alloc", "vsb_host_free",
+    "vsb_host_alloc", "vsb_host_free", "vsb_debug_read_global",
 )
 
 
@@ -96,6 +96,7 @@ class PlanInfo(ctypes.Structure):
         ("cluster", ctypes.c_int32),
         ("remote_stores", ctypes.c_int64),
         ("code_bytes", ctypes.c_int64),
+        ("n_cse", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -151,6 +152,7 @@ def lib() -> ctypes.CDLL:
     L.vsb_launches_per_eval.restype = i64
     L.vsb_host_alloc.argtypes = [ctypes.POINTER(vp), i64]
     L.vsb_host_free.argtypes = [vp]
+    L.vsb_debug_read_global.argtypes = [vp, i32, ctypes.c_char_p, i32, vp, i64]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int:  # default restype: status code

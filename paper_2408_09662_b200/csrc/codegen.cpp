@@ -47,6 +47,79 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
     nodes.reserve(static_cast<size_t>(n_rows));
 
     auto slot_ok = [&](int64_t s) { return s >= 0 && s < n_w; };
+
+    // Exact global value numbering.  An arithmetic row whose (op, operand values) pair was
+    // already computed reuses that value: every op is a deterministic function of its operand
+    // bits, so the result is bit-identical.  ADD and MUL operands are ordered (IEEE + and *
+    // commute exactly; NaN payloads are not part of the contract); FMIN/FMAX are not, their
+    // signed-zero ties keep the first operand (_kernels.py:116-143).  Plus the identities that
+    // hold for every IEEE input, -0/+0, inf and NaN included: x*1 = x/1 = x - (+0) = x + (-0) = x,
+    // x*(-1) = x/(-1) = -x, -(-x) = x.  (x + 0 is not one: -0 + +0 = +0.)  No folding of
+    // constant operands: the reference evaluates those at run time with its libm.
+    struct VnKey {
+        uint64_t a, b;
+        bool operator==(const VnKey& o) const { return a == o.a && b == o.b; }
+    };
+    struct VnHash {
+        size_t operator()(const VnKey& k) const { return std::hash<uint64_t>()(k.a * 0x9e3779b97f4a7c15ULL ^ k.b); }
+    };
+    std::unordered_map<VnKey, int32_t, VnHash> vn;
+    vn.reserve(static_cast<size_t>(n_rows));
+    auto const_bits = [&](int32_t id, uint64_t bits) {
+        if (id < 0 || nodes[id].op != OP_CONST) return false;
+        uint64_t b;
+        std::memcpy(&b, &nodes[id].imm, 8);
+        return b == bits;
+    };
+    const uint64_t kOne = 0x3ff0000000000000ULL, kMinusOne = 0xbff0000000000000ULL;
+    const uint64_t kPlusZero = 0, kMinusZero = 0x8000000000000000ULL;
+    std::function<int32_t(Node)> gvn = [&](Node nd) -> int32_t {
+        const int32_t x = nd.arg[0], y = nd.arg[1];
+        switch (nd.op) {
+        case OP_MUL:
+            if (const_bits(y, kOne)) return x;
+            if (const_bits(x, kOne)) return y;
+            if (const_bits(y, kMinusOne) || const_bits(x, kMinusOne)) {
+                Node ng;
+                ng.op = OP_NEG;
+                ng.arg[0] = const_bits(y, kMinusOne) ? x : y;
+                return gvn(ng);
+            }
+            break;
+        case OP_DIV:
+            if (const_bits(y, kOne)) return x;
+            if (const_bits(y, kMinusOne)) {
+                Node ng;
+                ng.op = OP_NEG;
+                ng.arg[0] = x;
+                return gvn(ng);
+            }
+            break;
+        case OP_SUB:
+            if (const_bits(y, kPlusZero)) return x;
+            break;
+        case OP_ADD:
+            if (const_bits(y, kMinusZero)) return x;
+            if (const_bits(x, kMinusZero)) return y;
+            break;
+        case OP_NEG:
+            if (nodes[x].op == OP_NEG) return nodes[x].arg[0];
+            break;
+        default:
+            break;
+        }
+        if ((nd.op == OP_ADD || nd.op == OP_MUL) && nd.arg[1] < nd.arg[0]) std::swap(nd.arg[0], nd.arg[1]);
+        const VnKey key{(static_cast<uint64_t>(nd.op) << 32) | static_cast<uint32_t>(nd.arg[0]),
+                        (static_cast<uint64_t>(static_cast<uint32_t>(nd.arg[1])) << 32) |
+                            static_cast<uint32_t>(nd.arg[2])};
+        auto it = vn.find(key);
+        if (it != vn.end()) return it->second;
+        nodes.push_back(nd);
+        const int32_t id = static_cast<int32_t>(nodes.size() - 1);
+        vn.emplace(key, id);
+        return id;
+    };
+
     for (int64_t r = 0; r < n_rows; ++r) {
         const int32_t* row = code + 5 * r;
         const int op = row[0], o = row[1], a = row[2], b = row[3];
@@ -107,9 +180,8 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
                 if (slot[s] < 0) return row_err(r, "work slot read before any write");
                 nd.arg[k] = slot[s];
             }
-            nodes.push_back(nd);
-            slot[o] = static_cast<int32_t>(nodes.size() - 1);
             ++p.n_arith_rows;
+            slot[o] = gvn(nd);
             break;
         }
         }
@@ -134,6 +206,9 @@ std::string build_program(const int32_t* code, const double* values, int64_t n_r
                 zero_node = it->second;
                 break;
             }
+    // rows GVN answered with an existing value (each other arithmetic row made one node)
+    p.n_cse = p.n_arith_rows;
+    for (const Node& nd : nodes) if (nd.op > OP_ASSIGN) --p.n_cse;
     // dead-code elimination: only values reaching an output store survive
     const size_t N = nodes.size();
     std::vector<uint8_t> live(N, 0);
@@ -324,6 +399,24 @@ __device__ __forceinline__ void vs_bulk_store(void* dst, const void* src, unsign
 #define VS_BULK_WAIT_ALL() asm volatile("cp.async.bulk.wait_group 0;" ::: "memory")
 #define VS_FENCE_ASYNC() asm volatile("fence.proxy.async.shared::cta;" ::: "memory")
 #define VS_FENCE_MBAR_INIT() asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory")
+// lockstep cluster points of team kernels (launched as clusters): wait for the previous
+// relaxed arrival of the cluster (if any), arrive again -- CTAs drift at most a few phases
+__device__ __noinline__ void vs_ls_point(int wait) {
+    if (wait) asm volatile("barrier.cluster.wait;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __noinline__ void vs_ls_wait() { asm volatile("barrier.cluster.wait;" ::: "memory"); }
+// team phase barrier on an mbarrier (per-thread arrive + parity wait): not a .aligned
+// collective, so legal where the warps of a CTA reach different instructions, without the
+// divergence check and duplicated slow path ptxas wraps around a non-aligned barrier.sync.
+// Release/acquire at CTA scope order each thread's shared-memory stores before the others' loads.
+__device__ __forceinline__ void vs_pbar_sync(unsigned a, unsigned parity) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+                 "VS_PW_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra VS_PW_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
 // FMIN/FMAX: NaN loses, ties keep the first operand (_kernels.py:116-143) -- explicit
 // selects, not DMNMX, so signed-zero ties match the reference bit for bit
 __device__ __forceinline__ real vs_fmin(real x, real y) { return (x != x) ? y : (y != y) ? x : (x <= y) ? x : y; }
@@ -357,7 +450,188 @@ struct TeamSchedule {
 // of ~L cost units per warp.  Dependencies inside a phase are only allowed
 // within one warp (program order); cross-warp values are consumed in a later
 // phase (after the barrier that separates phases).
-TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W, int L, int prio, int Wl,
+// Local search over a phase schedule (after the greedy list schedule): move single ops
+// between warps and into the neighbouring phases while every dependency stays legal (an
+// operand from another warp must come from an earlier phase; from the same warp, from an
+// earlier or the same phase).  Objective, lexicographic: J = sum over phases of the maximum
+// warp load + xw * (cross-warp / per-warp operand loads + cross-warp stores), then the sum
+// of squared loads (balancing moves that do not yet lower a maximum).  Emptied phases are
+// removed.  Each accepted move lowers (J, squares) strictly, so the search terminates.
+static void refine_schedule(const Program& p, const std::vector<int32_t>& ids,
+                            const std::vector<std::vector<int32_t>>& succ, const std::vector<int32_t>& local, int W,
+                            TeamSchedule& ts, std::vector<int32_t>& warp_of, std::vector<int32_t>& phase_of) {
+    const size_t M = ids.size();
+    int P = ts.P;
+    if (M == 0 || W < 2 || P < 2) return;
+    static const double xw = getenv("VSB_HC_XW") ? atof(getenv("VSB_HC_XW")) : 1.0;
+    static const int max_pass = getenv("VSB_HC_PASSES") ? atoi(getenv("VSB_HC_PASSES")) : 40;
+    static const int hc_span = getenv("VSB_HC_SPAN") ? atoi(getenv("VSB_HC_SPAN")) : 1;
+    auto in_chunk = [&](int32_t u) { return u >= 0 && local[u] >= 0; };
+    std::vector<double> load(static_cast<size_t>(P) * W, 0.0);
+    auto L = [&](int ph, int w) -> double& { return load[static_cast<size_t>(ph) * W + w]; };
+    for (size_t i = 0; i < M; ++i) L(phase_of[ids[i]], warp_of[ids[i]]) += op_cost(p.nodes[ids[i]].op);
+    // consumers of every operand (in-chunk or not) by warp: uses[u] = list of consumer nodes
+    std::unordered_map<int32_t, std::vector<int32_t>> ext_uses;   // operands defined outside the chunk
+    auto preds_of = [&](int32_t v, int32_t* out) {
+        const Node& nd = p.nodes[v];
+        int n = 0;
+        for (int k = 0; k < kArity[nd.op]; ++k) {
+            const int32_t u = nd.arg[k];
+            if (p.nodes[u].op == OP_CONST) continue;
+            bool dup = false;
+            for (int k2 = 0; k2 < n; ++k2) dup |= out[k2] == u;
+            if (!dup) out[n++] = u;
+        }
+        return n;
+    };
+    for (size_t i = 0; i < M; ++i) {
+        int32_t pr[3];
+        const int n = preds_of(ids[i], pr);
+        for (int k = 0; k < n; ++k)
+            if (!in_chunk(pr[k])) ext_uses[pr[k]].push_back(ids[i]);
+    }
+    auto users = [&](int32_t u) -> const std::vector<int32_t>& {
+        if (in_chunk(u)) return succ[local[u]];
+        return ext_uses[u];
+    };
+    // number of users of u on warp w other than v
+    auto users_on = [&](int32_t u, int w, int32_t v) {
+        int c = 0;
+        for (int32_t s : users(u)) c += (s != v && warp_of[s] == w);
+        return c;
+    };
+    auto phase_max = [&](int ph) {
+        double m = 0.0;
+        for (int w = 0; w < W; ++w) m = std::max(m, L(ph, w));
+        return m;
+    };
+    std::vector<double> pmax(P);
+    for (int ph = 0; ph < P; ++ph) pmax[ph] = phase_max(ph);
+    // change of the transfer count when v moves from warp a to warp b (same or other phase)
+    auto dxfer = [&](int32_t v, int a, int b) {
+        if (a == b) return 0;
+        int d = 0;
+        int32_t pr[3];
+        const int n = preds_of(v, pr);
+        for (int k = 0; k < n; ++k) {
+            const int32_t u = pr[k];
+            const int pw = in_chunk(u) ? warp_of[u] : -1;   // -1: input / import, loaded per warp
+            if (pw != a && users_on(u, a, v) == 0) --d;
+            if (pw != b && users_on(u, b, v) == 0) ++d;
+            if (pw >= 0) {   // producer-side store: exists while any user is on another warp
+                bool before = false, after = false;
+                for (int32_t s : succ[local[u]]) {
+                    const int ws = s == v ? a : warp_of[s];
+                    const int wn = s == v ? b : warp_of[s];
+                    before |= ws != pw;
+                    after |= wn != pw;
+                }
+                d += static_cast<int>(after) - static_cast<int>(before);
+            }
+        }
+        // v as a producer: distinct consumer warps other than its own, and its store
+        if (!succ[local[v]].empty()) {
+            uint64_t seen = 0;
+            for (int32_t s : succ[local[v]]) seen |= 1ULL << warp_of[s];
+            const int before = __builtin_popcountll(seen & ~(1ULL << a)), after = __builtin_popcountll(seen & ~(1ULL << b));
+            d += (after - before) + (static_cast<int>(after > 0) - static_cast<int>(before > 0));
+        }
+        return d;
+    };
+    auto legal = [&](int32_t v, int w2, int p2) {
+        int32_t pr[3];
+        const int n = preds_of(v, pr);
+        for (int k = 0; k < n; ++k) {
+            const int32_t u = pr[k];
+            if (!in_chunk(u)) continue;
+            if (phase_of[u] > p2 || (phase_of[u] == p2 && warp_of[u] != w2)) return false;
+        }
+        for (int32_t s : succ[local[v]])
+            if (phase_of[s] < p2 || (phase_of[s] == p2 && warp_of[s] != w2)) return false;
+        return true;
+    };
+    int64_t moves = 0;
+    for (int pass = 0; pass < max_pass; ++pass) {
+        int64_t pass_moves = 0;
+        for (int ph = 0; ph < P; ++ph) {
+            for (int guard = 0; guard < 4 * W; ++guard) {
+                // the most loaded warp of this phase
+                int wm = 0;
+                for (int w = 1; w < W; ++w) if (L(ph, w) > L(ph, wm)) wm = w;
+                if (L(ph, wm) <= 0.0) break;
+                bool moved = false;
+                auto& sq = ts.seq[wm][ph];
+                for (size_t i = 0; i < sq.size() && !moved; ++i) {
+                    const int32_t v = sq[i];
+                    const double c = op_cost(p.nodes[v].op);
+                    double best = 0.0, best_ss = 0.0;
+                    int bw = -1, bp = -1;
+                    for (int p2 = std::max(0, ph - hc_span); p2 <= std::min(P - 1, ph + hc_span); ++p2)
+                        for (int w2 = 0; w2 < W; ++w2) {
+                            if (p2 == ph && w2 == wm) continue;
+                            const double lt = L(p2, w2);
+                            // objective change: phase maxima
+                            double dj;
+                            L(ph, wm) -= c;
+                            L(p2, w2) += c;
+                            if (p2 == ph) dj = phase_max(ph) - pmax[ph];
+                            else dj = (phase_max(ph) - pmax[ph]) + (phase_max(p2) - pmax[p2]);
+                            L(ph, wm) += c;
+                            L(p2, w2) -= c;
+                            if (dj > 1e-9) continue;
+                            if (!legal(v, w2, p2)) continue;
+                            dj += xw * dxfer(v, wm, w2);
+                            const double lm = L(ph, wm);
+                            const double dss = (lm - c) * (lm - c) - lm * lm + (lt + c) * (lt + c) - lt * lt;
+                            if (dj < best - 1e-9 || (dj <= best + 1e-9 && dj <= 1e-9 && dss < best_ss - 1e-9)) {
+                                if (dj > 1e-9 || (dj > -1e-9 && dss >= -1e-9)) continue;
+                                best = dj; best_ss = dss; bw = w2; bp = p2;
+                            }
+                        }
+                    if (bw < 0) continue;
+                    // apply
+                    L(ph, wm) -= c;
+                    L(bp, bw) += c;
+                    warp_of[v] = bw;
+                    phase_of[v] = bp;
+                    sq.erase(sq.begin() + static_cast<long>(i));
+                    auto& dst = ts.seq[bw][bp];
+                    dst.insert(std::upper_bound(dst.begin(), dst.end(), v), v);
+                    pmax[ph] = phase_max(ph);
+                    pmax[bp] = phase_max(bp);
+                    moved = true;
+                    ++pass_moves;
+                }
+                if (!moved) break;
+            }
+        }
+        moves += pass_moves;
+        if (pass_moves == 0) break;
+    }
+    // drop emptied phases
+    std::vector<int32_t> newp(P, -1);
+    int np = 0;
+    for (int ph = 0; ph < P; ++ph) {
+        bool any = false;
+        for (int w = 0; w < W && !any; ++w) any = !ts.seq[w][ph].empty();
+        if (any) newp[ph] = np++;
+    }
+    if (np < P) {
+        for (int w = 0; w < W; ++w) {
+            std::vector<std::vector<int32_t>> ns(np);
+            for (int ph = 0; ph < P; ++ph) if (newp[ph] >= 0) ns[newp[ph]] = std::move(ts.seq[w][ph]);
+            ts.seq[w] = std::move(ns);
+        }
+        for (size_t i = 0; i < M; ++i) phase_of[ids[i]] = newp[phase_of[ids[i]]];
+    }
+    ts.P = np;
+    ts.makespan = 0.0;
+    for (int ph = 0; ph < P; ++ph) if (newp[ph] >= 0) ts.makespan += pmax[ph];
+    static const bool dbg = getenv("VSB_SCHED_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "refine: %lld moves, phases %d -> %d, makespan %.0f\n", (long long)moves, P, np, ts.makespan);
+}
+
+TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W, int L, int prio, int Wl, bool refine,
                            std::vector<int32_t>& warp_of, std::vector<int32_t>& phase_of) {
     TeamSchedule ts;
     ts.W = W;
@@ -420,6 +694,12 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
         for (double l : load) { mx = std::max(mx, l); sum += l; }
         if (dbg) fprintf(stderr, "phase %d: max %.0f mean %.1f deferred %zu ready %zu\n", phase, mx, sum / W,
                          deferred.size(), ready.size());
+        static const bool dump = getenv("VSB_SCHED_LOADS") != nullptr;
+        if (dump) {
+            fprintf(stderr, "loads %d:", phase);
+            for (double l : load) fprintf(stderr, " %.0f", l);
+            fprintf(stderr, "\n");
+        }
         ts.makespan += mx;
         ++phase;
         std::fill(load.begin(), load.end(), 0.0);
@@ -482,8 +762,15 @@ TeamSchedule schedule_team(const Program& p, int64_t first, int64_t last, int W,
     double mx = 0.0;
     for (double l : load) mx = std::max(mx, l);
     ts.makespan += mx;
+    if (getenv("VSB_SCHED_LOADS")) {
+        fprintf(stderr, "loads %d:", phase);
+        for (double l : load) fprintf(stderr, " %.0f", l);
+        fprintf(stderr, "\n");
+    }
     ts.P = phase + 1;
     for (auto& v : ts.seq) v.resize(ts.P);
+    static const int hc_env = getenv("VSB_HC") ? atoi(getenv("VSB_HC")) : 1;
+    if (refine && hc_env > 0 && !ranked) refine_schedule(p, ids, succ, local, W, ts, warp_of, phase_of);
     return ts;
 }
 
@@ -544,6 +831,10 @@ private:
     // team mode, rematerialised reloads: current version of a value's name in the warp being
     // emitted (0 = "v<u>", k = "v<u>_<k>")
     std::vector<int32_t> ver_;
+    // fp64 constants whose low 32 bits are not zero live in a __constant__ table: DADD / DMUL /
+    // DFMA read them as c[bank][offset] operands, where an inline literal costs two UMOVs per use
+    // (k_index_[u] = table index of CONST node u, -1 = literal)
+    std::vector<int32_t> k_index_;
 
     void cut_chunks();
     void plan_cross_chunk();
@@ -723,6 +1014,22 @@ void Emitter::build_header() {
     ks.groups = TG;
     ks.cluster = TK;
     ks.lockstep = (team && TK == 1 && opt.lockstep > 1) ? opt.lockstep : 1;   // grid: whole clusters
+    static const int ktab_env = getenv("VSB_CONST_TABLE") ? atoi(getenv("VSB_CONST_TABLE")) : 1;
+    k_index_.assign(N, -1);
+    if (!f32 && ktab_env) {
+        std::string tab;
+        int nk = 0;
+        for (int64_t q = 0; q < N && nk < 4096; ++q) {
+            const Node& nd = p.nodes[q];
+            if (nd.op != OP_CONST || !std::isfinite(nd.imm)) continue;
+            uint64_t bits;
+            std::memcpy(&bits, &nd.imm, 8);
+            if ((bits & 0xffffffffULL) == 0) continue;   // the DP immediate form holds the high word
+            k_index_[q] = nk++;
+            tab += (nk > 1 ? ", " : "") + literal(nd.imm, false);
+        }
+        if (nk > 0) hdr.put("__constant__ double vs_k[%d] = {%s};\n", nk, tab.c_str());
+    }
     // A/B knob: VSB_BAR_ALIGNED=1 emits the (formally undefined here) aligned bar.sync
     static const int bar_aligned = getenv("VSB_BAR_ALIGNED") ? atoi(getenv("VSB_BAR_ALIGNED")) : 0;
     if (bar_aligned) hdr.put("#define VS_BAR_ALIGNED %d\n", bar_aligned);
@@ -790,13 +1097,16 @@ void Emitter::build_header() {
                  "struct vs_sc { double s, c; };\n"
                  "__device__ __noinline__ vs_sc vs_sincos_o(double x) { vs_sc r; vs_sincos(x, &r.s, &r.c); return r; }\n";
     hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
-            "    long long e0, n, ld, io_ld, ipc;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
-    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc";
+            "    long long e0, n, ld, io_ld, ipc, flags;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
+    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc, flags";
 }
 
 std::string Emitter::opnd(int32_t u) const {
     const Node& nu = p.nodes[u];
-    if (nu.op == OP_CONST) return literal(nu.imm, f32);
+    if (nu.op == OP_CONST) {
+        if (!k_index_.empty() && k_index_[u] >= 0) return "vs_k[" + std::to_string(k_index_[u]) + "]";
+        return literal(nu.imm, f32);
+    }
     if (!ver_.empty() && ver_[u] > 0) return "v" + std::to_string(u) + "_" + std::to_string(ver_[u]);
     return "v" + std::to_string(u);
 }
@@ -1212,7 +1522,7 @@ void Emitter::emit_team_chunk(int c, Chunk& ch, Out& b) {
     tp.warp_of.assign(N, -1);
     tp.phase_of.assign(N, -1);
     tp.ts = schedule_team(p, ch.first, ch.last, tp.W, std::max(1, opt.phase_cost), opt.priority,
-                          tp.K > 1 ? tp.Wl : 0, tp.warp_of, tp.phase_of);
+                          tp.K > 1 ? tp.Wl : 0, opt.refine, tp.warp_of, tp.phase_of);
     tp.P = tp.ts.P;
     ch.phases = tp.P;
     team_barrier_plan(tp, ch);
@@ -1607,6 +1917,10 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     // lockstep kernels carry no compile-time cluster shape: the runtime launches them as
     // clusters of LS CTAs when the grid spans several waves and plainly (implicit 1-CTA
     // clusters, where the cluster barrier is a CTA barrier) otherwise
+    // VSB_PHASE_TRACE=1 (diagnostic): lane 0 of every warp of CTA 0 records clock64() when it
+    // reaches each phase barrier and when it leaves it; read back with vsb_debug_read_global
+    static const bool ptrace = getenv("VSB_PHASE_TRACE") && atoi(getenv("VSB_PHASE_TRACE")) != 0;
+    if (ptrace) b.put("__device__ unsigned long long vs_ptrace[%lld];\n", (long long)(2 * W * P + W));
     if (K > 1)
         b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n",
               K, opt.min_blocks, nbuf);
@@ -1624,6 +1938,7 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
         b.put("    const long long cid = (long long)blockIdx.x;\n");
     }
     b.put("    const int warp = crank * %d + wid %% %d;\n", Wl, Wl);
+    if (LS > 1 && !split) b.put("    const bool ls = (A.flags & 1) != 0;   // launched as lockstep clusters\n");
     // A.ipc <= VS_IPB instances per cluster (the runtime shrinks it so that the
     // grid fills whole waves of SMs; the spare lanes idle)
     // spare lanes mirror the last instance (identical bits; benign duplicate stores)
@@ -1645,13 +1960,31 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
         // every CTA of the cluster must be running before the first DSMEM store
         b.put("    VS_CBAR();\n");
     }
+    // phase barrier form: mbarrier (default) or barrier.sync (VSB_BAR_MBAR=0 / VSB_BAR_ALIGNED)
+    // measured (profiles/r2_sweeps_r08_defaults.jsonl): barrier.sync 0.416 vs mbarrier 0.433 ms on
+    // srbm_mpc B=4096 (the TRYWAIT wake-up is slower than the barrier unit's release); mixed
+    // elsewhere (humanoid_rbd B=4096 0.057 vs 0.055).  VSB_BAR_MBAR=1 selects the mbarrier form
+    static const int mbar_env = getenv("VSB_BAR_MBAR") ? atoi(getenv("VSB_BAR_MBAR")) : 0;
+    static const bool bar_aligned_env = getenv("VSB_BAR_ALIGNED") && atoi(getenv("VSB_BAR_ALIGNED")) != 0;
+    const bool mbar = K == 1 && !split && mbar_env != 0 && !bar_aligned_env && P > 1;
+    if (mbar) {
+        b.put("    __shared__ unsigned long long vs_pbar;\n");
+        b.put("    if (threadIdx.x == 0) vs_mbar_init(&vs_pbar, VS_BS);\n");
+        b.put("    __syncthreads();   // every thread, same instruction: before the per-warp switch\n");
+        b.put("    const unsigned vs_pb = vs_sa(&vs_pbar);\n");
+    }
+    if (ptrace) {
+        b.put("    const bool vs_trc = blockIdx.x == 0 && lane == 0;\n");
+        b.put("    if (vs_trc) vs_ptrace[%lld + warp] = clock64();\n", (long long)(2 * W * P));
+    }
     b.put("    switch (warp) {\n");
     std::vector<int32_t> have(N, -1);  // stamp = warp id for values available in this warp
     // rematerialisation (VSB_REMAT_GAP=g > 0): an input or a value imported from an earlier
     // chunk that this warp last touched more than g of its ops ago is loaded again (from the
     // input row / the chunk scratch, both read-only in this kernel) instead of being held in a
     // register across the gap -- fewer registers live, fewer ptxas spills
-    static const int remat_gap = getenv("VSB_REMAT_GAP") ? atoi(getenv("VSB_REMAT_GAP")) : 0;
+    static const int remat_env = getenv("VSB_REMAT_GAP") ? atoi(getenv("VSB_REMAT_GAP")) : -1;
+    const int remat_gap = remat_env >= 0 ? remat_env : opt.remat_gap;
     std::vector<int64_t> lastpos(N, 0);
     ver_.assign(N, 0);
     int64_t pos = 0, remat_id = 0;
@@ -1740,20 +2073,23 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
                 if (last)
                     for (int32_t s : stores_of[q]) emit_store(b, s, "v" + std::to_string(q), ind, false);
             }
+            if (ptrace) b.put("%sif (vs_trc) vs_ptrace[%lld] = clock64();\n", ind, (long long)(2 * (ph * W + w)));
             if (split) {
                 if (end_act[w][ph]) b.put(end_act[w][ph] == 2 ? "%sVS_BSYNC(%d);\n" : "%sVS_BARV(%d);\n", ind,
                                           1 + (ph - 1) % 15);
             } else if (ph + 1 < P) {
-                b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
+                if (mbar) b.put("%svs_pbar_sync(vs_pb, %du);\n", ind, ph & 1);
+                else b.put(K > 1 ? "%sVS_CBAR();\n" : "%sVS_BAR();\n", ind);
+                if (ptrace) b.put("%sif (vs_trc) vs_ptrace[%lld] = clock64();\n", ind, (long long)(2 * (ph * W + w) + 1));
             }
             // lockstep: every LE phases wait for the previous relaxed cluster arrival, arrive again
             // (the CTAs of a cluster drift at most LE phases apart); a last wait before exit
-            if (LS > 1 && !split && (ph + 1) % LE == 0 && ph + 1 < P) {
-                if (ph + 1 > LE) b.put("%sasm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n", ind);
-                b.put("%sasm volatile(\"barrier.cluster.arrive.relaxed;\" ::: \"memory\");\n", ind);
-            }
+            // (out-of-line calls: the straight-line stream carries a predicated CALL, not the
+            // barrier sequences and their divergence handling)
+            if (LS > 1 && !split && (ph + 1) % LE == 0 && ph + 1 < P)
+                b.put("%sif (ls) vs_ls_point(%d);\n", ind, ph + 1 > LE ? 1 : 0);
         }
-        if (LS > 1 && !split && P > LE) b.put("%sasm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n", ind);
+        if (LS > 1 && !split && P > LE) b.put("%sif (ls) vs_ls_wait();\n", ind);
         b.put("        break;\n    }\n");
     }
     b.put("    }\n}\n");

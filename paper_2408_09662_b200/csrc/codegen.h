@@ -48,6 +48,7 @@ struct Program {
     int64_t n_arith_rows = 0;     // rows other than CONST/INPUT/OUTPUT/ASSIGN
     int64_t n_live_ops = 0;       // live arithmetic SSA values after DCE
     int64_t n_dead = 0;           // arithmetic values removed by DCE
+    int64_t n_cse = 0;            // arithmetic rows answered by an existing value (exact GVN)
     int64_t n_zero_stores = 0;    // output nonzeros no OUTPUT row writes (stored as +0.0)
 };
 
@@ -74,6 +75,13 @@ struct EmitOptions {
     // values travel through shared memory.  0 = one thread per instance.
     int team = 0;
     int phase_cost = 96;       // cost units per warp per phase (team mode)
+    // team mode: refine the greedy phase schedule by local search (schedule_team ->
+    // refine_schedule); the runtime's width heuristic reads an unrefined dry schedule
+    bool refine = true;
+    // team mode: an input or a value imported from an earlier chunk that a warp last touched more
+    // than remat_gap of its ops ago is loaded again instead of held in a register (0 = never;
+    // VSB_REMAT_GAP overrides)
+    int remat_gap = 0;
     int priority = 0;          // team list-scheduling priority: 0 program order, 1 critical path
     int64_t team_smem = 200 * 1024;  // bytes of smem for cross-warp values (team mode)
     // groups: G 32-instance groups per CTA execute the same warp code (warp =

@@ -245,12 +245,18 @@ struct vsb_plan {
     std::map<int, HostWs> host_ws;
     std::set<int> pool_ready;
     std::string last_log;
+    // batch-adaptive shape (auto team plans of >= 40k-op tapes): calls of >= wide_min instances
+    // run a second variant, 8-warp teams x 2 instance groups per CTA (each fetched instruction
+    // issued for 64 instances) with rematerialised reloads; one-wave batches keep 16-warp teams
+    bool wide_ok = false;
+    int64_t wide_min = 0;
     int rsz() const { return opts.dtype == VSB_F32 ? 4 : 8; }
 };
 
 namespace {
 
 constexpr int kRollKey = 1 << 20;
+constexpr int kWideKey = 1 << 30;   // | AoS/SoA layout: the large-batch team shape
 
 int build_variant(vsb_plan* p, int layout, Variant** out) {
     auto it = p->variants.find(layout);
@@ -260,10 +266,12 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     }
     auto v = std::make_unique<Variant>();
     vsb::EmitOptions eo;
+    const bool wide = (layout & kWideKey) != 0;
+    const int base_layout = layout & ~kWideKey;
     eo.f32 = p->opts.dtype == VSB_F32;
-    eo.layout = layout == VSB_SOA ? vsb::Layout::SOA : vsb::Layout::AOS;
+    eo.layout = base_layout == VSB_SOA ? vsb::Layout::SOA : vsb::Layout::AOS;
     // rollout variants (vsb_rollout_device): key kRollKey + state_in * 65536 + state_out
-    const bool roll = layout >= kRollKey;
+    const bool roll = !wide && layout >= kRollKey;
     if (roll) {
         eo.roll_in = (layout - kRollKey) / 65536;
         eo.roll_out = (layout - kRollKey) % 65536;
@@ -283,6 +291,13 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     eo.team_smem = p->opts.team_smem;
     eo.groups = p->opts.groups;
     eo.cluster = p->opts.cluster;
+    if (wide) {
+        // srbm_mpc B=65536: 6.03 (16 warps) -> 5.49 ms, B=262144: 24.4 -> 22.2 ms
+        // (profiles/r2_sweeps_r08_defaults.jsonl)
+        eo.team = 8;
+        eo.groups = 2;
+        eo.remat_gap = 256;
+    }
     eo.bulk_io = p->opts.bulk_io >= 0 && !roll;
     // outlined subroutines (bit 0 DIV, bit 1 SIN/COS, bit 2 EXP/LOG/POW/TAN/ATAN2): team kernels
     // are instruction-fetch bound and outline DIV + SIN/COS; any plan outlines SIN/COS and the
@@ -325,7 +340,8 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     if (eo.outline) shape += "o" + std::to_string(eo.outline);
     if (!eo.bulk_io) shape += "nb";
     if (roll) shape += "r" + std::to_string(eo.roll_in) + "_" + std::to_string(eo.roll_out);
-    v->ks = vsb::emit(p->prog, eo, p->tag + (layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
+    if (eo.remat_gap > 0) shape += "m" + std::to_string(eo.remat_gap);
+    v->ks = vsb::emit(p->prog, eo, p->tag + (base_layout == VSB_SOA ? "s" : "a") + (eo.f32 ? "f" : "d") + shape);
 
     // -lineinfo embeds the whole PTX text in the cubin (2-3x its size; the in-tree cache
     // travels to the GPU box), so it is on only for profiling runs: VSB_LINEINFO=1
@@ -365,6 +381,12 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
     *out = v.get();
     p->variants[layout] = std::move(v);
     return VSB_OK;
+}
+
+// the variant a call of n instances runs (AoS / SoA; the large-batch shape when eligible)
+int pick_variant(vsb_plan* p, int layout, int64_t n, Variant** out) {
+    if (p->wide_ok && n >= p->wide_min && (layout == VSB_AOS || layout == VSB_SOA)) layout |= kWideKey;
+    return build_variant(p, layout, out);
 }
 
 int sm_count(int device);
@@ -517,7 +539,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             if (p->prog.nnz_out[j]) use = ((reinterpret_cast<uintptr_t>(outs[j]) + e0 * p->prog.nnz_out[j] * rs) & 15) == 0;
         if (use) {
             const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
-            std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
+            std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
             for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
             for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
             const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -549,7 +571,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
         ensure_pool(p, device);
         CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(ld_max * v->ks.scratch_slots * p->rsz()), stream));
     }
-    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
     for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
     for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -568,7 +590,11 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             const auto& ch = v->ks.chunks[c];
             const int64_t grid = units_for(v->ks, m, n_sm) * ch.cluster;
             cudaError_t e;
-            if (v->ks.lockstep > 1 && grid > n_sm) {
+            // flags bit 0: launched as lockstep clusters (the kernels' cluster barriers run only
+            // then; a one-wave launch skips them, and with them their L1-invalidating acquire)
+            const bool clustered = v->ks.lockstep > 1 && grid > n_sm;
+            pb[base + 6] = clustered ? 1u : 0u;
+            if (clustered) {
                 // several waves: pairs (lockstep) of CTAs share a cluster and meet at a relaxed
                 // cluster barrier every few phases -- their identical instruction streams stay
                 // together (humanoid_rbd B=65536: 0.94 -> 0.71 ms, profiles/r2_summary.md)
@@ -707,11 +733,17 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
         dry.chunk_ops = p->opts.chunk_ops < 0 ? (int64_t)1 << 60 : p->opts.chunk_ops;
         dry.team_smem = p->opts.team_smem;
         dry.phase_cost = p->opts.phase_cost;
+        dry.refine = false;   // the thresholds below were measured on greedy schedules
         // and mid-width ones with 12 (ldlt_57, live sum 1456: team 12 / 16 = 0.377 / 0.427 ms at
         // B=4096; srbm_mpc 1104 keeps 16: 0.410 / 0.433; profiles/r1_sweeps_r50_team_width.jsonl)
         const int64_t live16 = vsb::emit(p->prog, dry, "dry").live_total;
         if (live16 > 1500) p->opts.team = 8;
         else if (live16 > 1200) p->opts.team = 12;
+    }
+    if (team_auto && p->opts.team == 16 && p->opts.groups == 1 && p->opts.cluster == 1) {
+        static const int64_t env_wide = getenv("VSB_WIDE_MIN") ? atoll(getenv("VSB_WIDE_MIN")) : -1;
+        p->wide_ok = env_wide != 0;
+        p->wide_min = env_wide > 0 ? env_wide : 8 * 148 * 32;   // >= 8 waves of 16-warp team CTAs
     }
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
@@ -750,6 +782,7 @@ int vsb_plan_get_info(vsb_plan* p, vsb_plan_info* info) {
     info->n_rows = p->prog.n_rows;
     info->n_arith_rows = p->prog.n_arith_rows;
     info->n_live_ops = p->prog.n_live_ops;
+    info->n_cse = p->prog.n_cse;
     info->n_chunks = static_cast<int64_t>(v->ks.chunks.size());
     info->scratch_slots = v->ks.scratch_slots;
     for (auto& ch : v->ks.chunks) {
@@ -804,6 +837,24 @@ int vsb_plan_source(vsb_plan* p, int32_t chunk, const char** src) {
     return VSB_OK;
 }
 
+int vsb_debug_read_global(vsb_plan* p, int32_t chunk, const char* name, int32_t device, void* host, int64_t bytes) {
+    if (!p || !name || !host || bytes < 0) return fail(VSB_ERR_INVALID, "null argument");
+    DEVICE_GUARD(device);
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->variants.find(VSB_AOS);
+    if (it == p->variants.end() || !it->second) return fail(VSB_ERR_INVALID, "plan has no AoS variant");
+    Variant* v = it->second.get();
+    int rc = ensure_loaded(v, device);
+    if (rc != VSB_OK) return rc;
+    if (chunk < 0 || chunk >= static_cast<int32_t>(v->libs.size())) return fail(VSB_ERR_INVALID, "chunk out of range");
+    void* dptr = nullptr;
+    size_t size = 0;
+    CUDA_TRY(cudaLibraryGetGlobal(&dptr, &size, v->libs[chunk], name));
+    if (static_cast<size_t>(bytes) > size) return fail(VSB_ERR_INVALID, "global is smaller than the requested bytes");
+    CUDA_TRY(cudaMemcpy(host, dptr, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost));
+    return VSB_OK;
+}
+
 int vsb_plan_log(vsb_plan* p, const char** log) {
     if (!p || !log) return fail(VSB_ERR_INVALID, "null argument");
     *log = p->last_log.c_str();
@@ -813,7 +864,8 @@ int vsb_plan_log(vsb_plan* p, const char** log) {
 int64_t vsb_launches_per_eval(vsb_plan* p, int64_t n) {
     if (!p || n <= 0) return 0;
     std::lock_guard<std::mutex> lk(p->mu);
-    Variant* v = p->variants.at(VSB_AOS).get();
+    Variant* v = nullptr;
+    if (pick_variant(p, VSB_AOS, n, &v) != VSB_OK) return 0;
     if (v->tma_kern && !getenv("VSB_NO_TMA")) {
         auto g = v->tma_grid.begin();
         if (g != v->tma_grid.end() && (p->opts.bulk_io > 0 || n / v->ks.chunks[0].threads >= 3 * g->second))
@@ -834,7 +886,7 @@ int vsb_eval_device(vsb_plan* p, const void* in_buf, const int64_t* in_off, void
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
-        rc = build_variant(p, VSB_AOS, &v);
+        rc = pick_variant(p, VSB_AOS, e1 - e0, &v);
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
     }
     if (rc != VSB_OK) return rc;
@@ -857,7 +909,7 @@ int vsb_eval_device_ptrs(vsb_plan* p, const void* const* ins_, void* const* outs
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
-        rc = build_variant(p, VSB_AOS, &v);
+        rc = pick_variant(p, VSB_AOS, e1 - e0, &v);
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
     }
     if (rc != VSB_OK) return rc;
@@ -892,7 +944,7 @@ int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const v
                                          "team plan, or a state nonzero the tape never stores)");
     const auto& ch = v->ks.chunks[0];
     const int64_t n = e1 - e0, BSz = ch.threads;
-    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 6), 0);
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
     for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins_[i]);
     for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs_[j]);
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -934,7 +986,7 @@ int vsb_eval_device_soa(vsb_plan* p, const void* const* ins_, void* const* outs_
     Variant* v;
     {
         std::lock_guard<std::mutex> lk(p->mu);
-        rc = build_variant(p, VSB_SOA, &v);
+        rc = pick_variant(p, VSB_SOA, e1 - e0, &v);
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
     }
     if (rc != VSB_OK) return rc;
@@ -956,7 +1008,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     std::vector<cudaStream_t> streams;  // [0] H2D, [1] D2H, [2..] one compute stream per piece
     {
         std::lock_guard<std::mutex> lk(p->mu);
-        rc = build_variant(p, VSB_AOS, &v);
+        rc = pick_variant(p, VSB_AOS, e1 - e0, &v);
         if (rc == VSB_OK) rc = ensure_loaded(v, device);
         if (rc != VSB_OK) return rc;
         auto& ss = p->streams[device];

@@ -555,3 +555,14 @@ def test_sharder_over_distinct_devices():
     for j, r in enumerate(ref):
         assert_close(ws.output_matrix(j), r, RTOL64, f"sharded over {n} GPUs out {j}")
     assert torch.cuda.current_device() == 0   # the device guard restored the caller's device
+
+
+def test_value_numbering_is_bitwise_on_special_values():
+    # the merged rows and identities hold for every IEEE class (signed zeros, subnormals,
+    # infinities, NaN): GPU == oracle (the reference's run_range restated) bit for bit
+    from vn_tapes import vn_inputs, vn_tape
+
+    tape, ins = vn_tape(), vn_inputs()
+    ref = oracle.batch_eval(tape, ins)
+    got = gpu_eval(tape, ins)
+    assert_bitwise_or_nan(got[0], ref[0], "value numbering")

@@ -156,3 +156,13 @@ def test_hoisted_split_is_memoised():
     a = rollout._split_of(t, 0)
     assert rollout._split_of(workloads.load_tape("quad_step"), 0) is a
     assert a.hoisted_rows == 42501
+
+
+def test_value_numbering_merges_only_exact_equivalences():
+    # exact GVN + IEEE identities (codegen.cpp build_program): counted without compiling
+    from vn_tapes import EXPECTED_CSE, vn_tape
+
+    p = Plan(vn_tape(), cache_dir="", compile_threads=-1)
+    assert p.info["n_cse"] == EXPECTED_CSE
+    # 16 arithmetic rows - 10 merged = 6 live ops: NEG x, x+y, x*y, fmin(x,y), fmin(y,x), x+0
+    assert p.info["n_live_ops"] == 6

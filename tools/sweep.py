@@ -44,15 +44,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--check", type=int, default=0)
     ap.add_argument("--env", nargs="*", default=[], help="KEY=VALUE environment settings (before plan creation)")
+    ap.add_argument("--compile-only", action="store_true",
+                    help="NVRTC-compile the plans into the cubin cache and print their statistics (no GPU)")
     args = ap.parse_args()
     for kv in args.env:
         k, v = kv.split("=", 1)
         os.environ[k] = v
 
-    import torch
-
     import paper_2408_09662_b200 as vsb
     import workloads
+
+    if args.compile_only:
+        for name in args.workload:
+            for opts in parse_grid(args.grid):
+                info = vsb.Plan(workloads.load_tape(name), **opts).info
+                print(json.dumps({"workload": name, "opts": opts, "env": args.env, "info": info}), flush=True)
+        return
+
+    import torch
 
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
