@@ -1100,9 +1100,8 @@ void Emitter::build_header() {
                  "struct vs_sc { double s, c; };\n"
                  "__device__ __noinline__ vs_sc vs_sincos_o(double x) { vs_sc r; vs_sincos(x, &r.s, &r.c); return r; }\n";
     hdr.put("struct VsArgs {\n    const real* in[%d];\n    real* out[%d];\n    real* scratch;\n"
-            "    long long e0, n, ld, io_ld, ipc, flags;\n"
-            "    const unsigned* wflag;\n    long long wbase, wrows, wseq;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
-    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc, flags, wflag, wbase, wrows, wseq";
+            "    long long e0, n, ld, io_ld, ipc, flags;\n};\n", std::max(n_in, 1), std::max(n_out, 1));
+    ks.arg_struct = "in[max(n_in,1)], out[max(n_out,1)], scratch, e0, n, ld, io_ld, ipc, flags";
 }
 
 std::string Emitter::opnd(int32_t u) const {
@@ -1950,23 +1949,6 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     b.put("    if (grp * 32 + lane >= A.ipc || t >= A.n) t = A.n - 1;\n");
     b.put("    const long long e = A.e0 + t;\n");
     b.put("    (void)e;\n");
-    // streamed inputs (host path, flags bit 1, first chunk only): the H2D copy arrives in
-    // sub-pieces, each followed by a 4-byte flag copy; the CTA starts once the sub-piece
-    // holding its last row has landed (copies run in order on one stream).  Bounded wait
-    // (~2 s): a failed copy is reported by the host, it does not hang the kernel
-    b.put("    if (A.flags & 2) {\n");
-    b.put("        if (threadIdx.x == 0) {\n");
-    b.put("            long long last = (cid + 1) * A.ipc; if (last > A.n) last = A.n;\n");
-    b.put("            const unsigned* f = A.wflag + (A.wbase + last - 1) / A.wrows;\n");
-    b.put("            unsigned got = 0;\n");
-    b.put("            for (int it = 0; it < (1 << 24); ++it) {\n");
-    b.put("                asm volatile(\"ld.acquire.gpu.global.u32 %%0, [%%1];\" : \"=r\"(got) : \"l\"(f) : \"memory\");\n");
-    b.put("                if (got == (unsigned)A.wseq) break;\n");
-    b.put("                __nanosleep(128);\n");
-    b.put("            }\n");
-    b.put("        }\n");
-    b.put("        __syncthreads();   // every thread, same instruction: before the per-warp switch\n");
-    b.put("    }\n");
     io_bases(b);
     b.put("    real* __restrict__ S = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32 + lane;\n");
     b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");

@@ -241,9 +241,6 @@ struct vsb_plan {
         std::unique_ptr<std::mutex> mu{new std::mutex};
         std::vector<cudaEvent_t> events;   // reused across calls (guarded by mu)
         int n_sm = 0;
-        unsigned* hseq = nullptr;          // pinned: the value the streamed-input flag copies write
-        uint32_t seq = 0;                  // per call (0 never used: flags are zeroed on allocation)
-        bool flags_zeroed = false;
     };
     std::map<int, HostWs> host_ws;
     std::set<int> pool_ready;
@@ -522,16 +519,8 @@ int64_t chain_scratch_bytes(vsb_plan* p, Variant* v, int64_t n, int n_sm) {
     return ld_max * v->ks.scratch_slots * p->rsz();
 }
 
-// streamed inputs of the host path (team plans): chunk 0's CTAs wait for flag[(row)/rows] == seq
-struct StreamIn {
-    const unsigned* flag = nullptr;
-    int64_t rows = 1;
-    uint32_t seq = 0;
-};
-
 int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, const std::vector<void*>& outs,
-                 int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device, void* scratch_pre = nullptr,
-                 const StreamIn* sin = nullptr) {
+                 int64_t e0, int64_t n, int64_t io_ld, cudaStream_t stream, int device, void* scratch_pre = nullptr) {
     if (n <= 0) return VSB_OK;
     // persistent TMA variant: full 128-instance tiles through the bulk-copy pipeline, the
     // partial tail inside the same launch.  Only when every resident CTA gets >= 3 tiles --
@@ -550,7 +539,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             if (p->prog.nnz_out[j]) use = ((reinterpret_cast<uintptr_t>(outs[j]) + e0 * p->prog.nnz_out[j] * rs) & 15) == 0;
         if (use) {
             const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
-            std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 11), 0);
+            std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
             for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
             for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
             const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -582,7 +571,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
         ensure_pool(p, device);
         CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(ld_max * v->ks.scratch_slots * p->rsz()), stream));
     }
-    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 11), 0);
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
     for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins[i]);
     for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs[j]);
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -604,14 +593,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             // flags bit 0: launched as lockstep clusters (the kernels' cluster barriers run only
             // then; a one-wave launch skips them, and with them their L1-invalidating acquire)
             const bool clustered = v->ks.lockstep > 1 && grid > n_sm;
-            const bool wait_in = sin && c == 0;
-            pb[base + 6] = (clustered ? 1u : 0u) | (wait_in ? 2u : 0u);
-            if (wait_in) {
-                pb[base + 7] = reinterpret_cast<uint64_t>(sin->flag);
-                pb[base + 8] = static_cast<uint64_t>(w0);   // rows of the call before this wave
-                pb[base + 9] = static_cast<uint64_t>(sin->rows);
-                pb[base + 10] = sin->seq;
-            }
+            pb[base + 6] = clustered ? 1u : 0u;
             if (clustered) {
                 // several waves: pairs (lockstep) of CTAs share a cluster and meet at a relaxed
                 // cluster barrier every few phases -- their identical instruction streams stay
@@ -780,7 +762,6 @@ int vsb_plan_destroy(vsb_plan* p) {
         cudaGetDevice(&prev);
         cudaSetDevice(kv.first);
         if (kv.second.base) cudaFree(kv.second.base);
-        if (kv.second.hseq) cudaFreeHost(kv.second.hseq);
         for (auto e : kv.second.events) cudaEventDestroy(e);
         cudaSetDevice(prev);
     }
@@ -965,7 +946,7 @@ int vsb_rollout_device(vsb_plan* p, int32_t state_in, int32_t state_out, const v
                                          "team plan, or a state nonzero the tape never stores)");
     const auto& ch = v->ks.chunks[0];
     const int64_t n = e1 - e0, BSz = ch.threads;
-    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 11), 0);
+    std::vector<uint64_t> pb(static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1) + 7), 0);
     for (int i = 0; i < n_in; ++i) pb[i] = reinterpret_cast<uint64_t>(ins_[i]);
     for (int j = 0; j < n_out; ++j) pb[std::max(n_in, 1) + j] = reinterpret_cast<uint64_t>(outs_[j]);
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
@@ -1075,21 +1056,6 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         off_scr[k] = total;
         total += align(chain_scratch_bytes(p, v, std::min(n, (k + 1) * piece) - k * piece, n_sm));
     }
-    // streamed inputs (team plans, one piece): the H2D copy goes in `sub` row ranges, each
-    // followed by a flag copy; the kernel chain is queued first and chunk 0's CTAs start as
-    // soon as the range holding their rows has landed, so the copy overlaps the first chunk
-    // (VSB_STREAM_IN=k sub-ranges, default 4; 0 or 1 = copy, then launch)
-    static const int stream_in_env = getenv("VSB_STREAM_IN") ? atoi(getenv("VSB_STREAM_IN")) : 4;
-    constexpr int kMaxSub = 16;
-    const int64_t IPB = v->ks.chunks.front().inst_per_block;
-    int64_t sub = 1, sub_rows = n;
-    if (v->ks.team >= 2 && pieces == 1 && n_in > 0 && p->prog.in_base[n_in] > 0 && stream_in_env > 1) {
-        sub = std::min<int64_t>({stream_in_env, kMaxSub, (n + IPB - 1) / IPB});
-        sub_rows = ((n + sub - 1) / sub + IPB - 1) / IPB * IPB;
-        sub = (n + sub_rows - 1) / sub_rows;
-    }
-    const int64_t off_flag = total;
-    total += align(kMaxSub * 4);
     vsb_plan::HostWs* ws;
     {
         std::lock_guard<std::mutex> lk(p->mu);
@@ -1102,9 +1068,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         ws->bytes = 0;
         CUDA_TRY(cudaMalloc(&ws->base, static_cast<size_t>(std::max<int64_t>(total, 256))));
         ws->bytes = static_cast<size_t>(std::max<int64_t>(total, 256));
-        ws->flags_zeroed = false;
     }
-    if (!ws->hseq) CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ws->hseq), 64, cudaHostAllocDefault));
     char* wb = static_cast<char*>(ws->base);
     std::vector<void*> d_in(n_in, nullptr), d_out(n_out, nullptr);
     for (int i = 0; i < n_in; ++i) if (p->prog.nnz_in[i]) d_in[i] = wb + off_in[i];
@@ -1123,15 +1087,6 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         cudaEventRecord(tev[0], sh);
     }
     cudaEvent_t alloc_done = ev[2 * pieces];
-    unsigned* dflag = reinterpret_cast<unsigned*>(wb + off_flag);
-    if (sub > 1) {
-        if (!ws->flags_zeroed) {   // stale flags never equal a later call's sequence number
-            CUDA_TRY(cudaMemsetAsync(dflag, 0, kMaxSub * 4, sh));
-            ws->flags_zeroed = true;
-        }
-        if (++ws->seq == 0) ws->seq = 1;
-        *ws->hseq = ws->seq;   // the previous call's flag copies completed before it returned
-    }
     cudaEventRecord(alloc_done, sh);
     cudaStreamWaitEvent(sd, alloc_done, 0);
     const char* hin = static_cast<const char*>(in_buf);
@@ -1174,37 +1129,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         return err;
     };
     const int ev_split = static_cast<int>(2 * pieces + 1);
-    std::vector<const void*> ins(n_in);
-    std::vector<void*> outs(n_out);
-    for (int i = 0; i < n_in; ++i) ins[i] = d_in[i];
-    for (int j = 0; j < n_out; ++j) outs[j] = d_out[j];
-    if (sub > 1 && rc == VSB_OK) {
-        // chain first (its CTAs wait on the flags), then the row ranges + flags on the copy stream
-        cudaStream_t sc = streams[2];
-        cudaStreamWaitEvent(sc, alloc_done, 0);
-        if (trace) cudaEventRecord(tev[1], sc);
-        StreamIn si;
-        si.flag = dflag;
-        si.rows = sub_rows;
-        si.seq = ws->seq;
-        rc = launch_chain(p, v, ins, outs, 0, n, 0, sc, device, v->ks.scratch_slots > 0 ? wb + off_scr[0] : nullptr, &si);
-        cudaEventRecord(ev[pieces], sc);
-        for (int64_t q = 0; q < sub && rc == VSB_OK; ++q) {
-            const int64_t lo = q * sub_rows, m = std::min(n, lo + sub_rows) - lo;
-            for (int i = 0; i < n_in && rc == VSB_OK; ++i) {
-                const int64_t nz = p->prog.nnz_in[i];
-                if (!nz) continue;
-                cudaError_t e = cudaMemcpyAsync(static_cast<char*>(d_in[i]) + lo * nz * rs,
-                                                hin + (in_off[i] + (e0 + lo) * nz) * rs, static_cast<size_t>(m * nz * rs),
-                                                cudaMemcpyHostToDevice, sh);
-                if (e != cudaSuccess) rc = fail(VSB_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
-            }
-            cudaError_t e = cudaMemcpyAsync(dflag + q, ws->hseq, 4, cudaMemcpyHostToDevice, sh);
-            if (e != cudaSuccess && rc == VSB_OK) rc = fail(VSB_ERR_CUDA, std::string("H2D flag: ") + cudaGetErrorString(e));
-        }
-        cudaEventRecord(ev[0], sh);
-    }
-    if (sub == 1 && one_in && p->prog.in_base[n_in] > 0) {
+    if (one_in && p->prog.in_base[n_in] > 0) {
         cudaError_t e = split_copy(wb + off_in[0], hin + (in_off[0] + e0 * p->prog.nnz_in[0]) * rs,
                                    static_cast<size_t>(n * p->prog.in_base[n_in] * rs), cudaMemcpyHostToDevice, sh,
                                    2 + kMaxPieces, ev_split);
@@ -1212,7 +1137,7 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         cudaEventRecord(ev[0], sh);
     }
     // 1. H2D of every piece, in order
-    for (int64_t k = 0; k < pieces && rc == VSB_OK && !one_in && sub == 1; ++k) {
+    for (int64_t k = 0; k < pieces && rc == VSB_OK && !one_in; ++k) {
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         for (int i = 0; i < n_in; ++i) {
             const int64_t nz = p->prog.nnz_in[i];
@@ -1225,7 +1150,11 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
         cudaEventRecord(ev[k], sh);
     }
     // 2. kernels per piece on their own stream
-    for (int64_t k = 0; k < pieces && rc == VSB_OK && sub == 1; ++k) {
+    std::vector<const void*> ins(n_in);
+    std::vector<void*> outs(n_out);
+    for (int i = 0; i < n_in; ++i) ins[i] = d_in[i];
+    for (int j = 0; j < n_out; ++j) outs[j] = d_out[j];
+    for (int64_t k = 0; k < pieces && rc == VSB_OK; ++k) {
         const int64_t lo = k * piece, m = std::min(n, lo + piece) - lo;
         cudaStream_t sc = streams[2 + k];
         cudaStreamWaitEvent(sc, ev[k], 0);

@@ -24,6 +24,8 @@ import oracle  # noqa: E402
 from paper_2408_09662_b200 import Function  # noqa: E402
 
 args = sys.argv[1:]
+host = "--host" in args   # through batch_eval (the host path: streamed H2D inputs for team plans)
+args = [a for a in args if a != "--host"]
 if args[0] == "--fuzz":
     from test_acceptance_fuzz import _golden, _tapes, inputs_for
 
@@ -39,7 +41,16 @@ else:
     ins = workloads.make_inputs(name, B, seed=5)
     opts = json.loads(args[2]) if len(args) > 2 else {}
 f = Function(tape, **opts)
-outs = f(*[torch.tensor(v, device="cuda") for v in ins])
+if host:
+    from paper_2408_09662_b200 import BatchWorkspace, batch_eval
+
+    ws = BatchWorkspace(tape, B)
+    for i, v in enumerate(ins):
+        ws.set_input(i, v)
+    batch_eval(tape, ws, plan_options=opts or None)
+    outs = [torch.tensor(ws.output_matrix(j).copy()) for j in range(tape.n_out)]
+else:
+    outs = f(*[torch.tensor(v, device="cuda") for v in ins])
 torch.cuda.synchronize()
 ref = oracle.batch_eval(tape, ins, n_threads=8)
 worst = 0.0
@@ -50,6 +61,6 @@ for o, r in zip(outs, ref):
     e[np.isnan(g) & np.isnan(r)] = 0
     worst = max(worst, float(np.nanmax(e)) if e.size else 0.0)
 info = f.plan.info
-print(json.dumps({"tape": tape.name, "batch": B, "opts": opts, "team": info["team"], "chunks": info["n_chunks"],
+print(json.dumps({"tape": tape.name, "batch": B, "opts": opts, "host": host, "team": info["team"], "chunks": info["n_chunks"],
                   "overflow_slots": info["overflow_slots"], "max_rel_err": worst}))
 sys.exit(0 if worst <= 1e-9 else 1)
