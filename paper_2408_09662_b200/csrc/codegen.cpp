@@ -1528,6 +1528,43 @@ void Emitter::emit_team_chunk(int c, Chunk& ch, Out& b) {
                           tp.K > 1 ? tp.Wl : 0, opt.refine, tp.warp_of, tp.phase_of);
     tp.P = tp.ts.P;
     ch.phases = tp.P;
+    // schedule legality (cheap; VSB_SCHED_CHECK=1 aborts on a violation): every in-chunk
+    // operand of an op comes from an earlier phase, or from the same warp earlier in the
+    // same phase
+    static const bool sched_check = getenv("VSB_SCHED_CHECK") && atoi(getenv("VSB_SCHED_CHECK")) != 0;
+    if (sched_check) {
+        std::vector<int64_t> pos(N, -1);
+        for (int w = 0; w < tp.W; ++w)
+            for (int ph = 0; ph < tp.P; ++ph) {
+                int64_t k = 0;
+                for (int32_t q : tp.ts.seq[w][ph]) {
+                    if (tp.warp_of[q] != w || tp.phase_of[q] != ph) {
+                        fprintf(stderr, "sched check: node %d listed at (w%d,p%d) but recorded (w%d,p%d)\n", q, w, ph,
+                                tp.warp_of[q], tp.phase_of[q]);
+                        abort();
+                    }
+                    pos[q] = k++;
+                }
+            }
+        for (int64_t q = ch.first; q < ch.last; ++q) {
+            const Node& nd = p.nodes[q];
+            if (nd.op <= OP_ASSIGN) continue;
+            if (pos[q] < 0) { fprintf(stderr, "sched check: node %lld unscheduled\n", (long long)q); abort(); }
+            for (int k = 0; k < kArity[nd.op]; ++k) {
+                const int32_t u = nd.arg[k];
+                if (!(u >= ch.first && u < ch.last && p.nodes[u].op > OP_ASSIGN)) continue;
+                const bool ok = tp.warp_of[u] == tp.warp_of[q]
+                                    ? (tp.phase_of[u] < tp.phase_of[q] || (tp.phase_of[u] == tp.phase_of[q] && pos[u] < pos[q]))
+                                    : tp.phase_of[u] < tp.phase_of[q];
+                if (!ok) {
+                    fprintf(stderr, "sched check: chunk %d node %lld (w%d,p%d,#%lld) reads %d (w%d,p%d,#%lld)\n", c,
+                            (long long)q, tp.warp_of[q], tp.phase_of[q], (long long)pos[q], u, tp.warp_of[u],
+                            tp.phase_of[u], (long long)pos[u]);
+                    abort();
+                }
+            }
+        }
+    }
     team_barrier_plan(tp, ch);
     team_cross_warp_values(tp, ch, c);
     team_rows(tp, ch);
@@ -1942,6 +1979,7 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     }
     b.put("    const int warp = crank * %d + wid %% %d;\n", Wl, Wl);
     if (LS > 1 && !split) b.put("    const bool ls = (A.flags & 1) != 0;   // launched as lockstep clusters\n");
+    static const bool ls_inline = getenv("VSB_LS_INLINE") && atoi(getenv("VSB_LS_INLINE")) != 0;
     // A.ipc <= VS_IPB instances per cluster (the runtime shrinks it so that the
     // grid fills whole waves of SMs; the spare lanes idle)
     // spare lanes mirror the last instance (identical bits; benign duplicate stores)
@@ -2089,10 +2127,18 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
             // (the CTAs of a cluster drift at most LE phases apart); a last wait before exit
             // (out-of-line calls: the straight-line stream carries a predicated CALL, not the
             // barrier sequences and their divergence handling)
-            if (LS > 1 && !split && (ph + 1) % LE == 0 && ph + 1 < P)
-                b.put("%sif (ls) vs_ls_point(%d);\n", ind, ph + 1 > LE ? 1 : 0);
+            if (LS > 1 && !split && (ph + 1) % LE == 0 && ph + 1 < P) {
+                if (ls_inline) {
+                    b.put("%sif (ls) {\n", ind);
+                    if (ph + 1 > LE) b.put("%s    asm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n", ind);
+                    b.put("%s    asm volatile(\"barrier.cluster.arrive.relaxed;\" ::: \"memory\");\n%s}\n", ind, ind);
+                } else {
+                    b.put("%sif (ls) vs_ls_point(%d);\n", ind, ph + 1 > LE ? 1 : 0);
+                }
+            }
         }
-        if (LS > 1 && !split && P > LE) b.put("%sif (ls) vs_ls_wait();\n", ind);
+        if (LS > 1 && !split && P > LE)
+            b.put(ls_inline ? "%sif (ls) asm volatile(\"barrier.cluster.wait;\" ::: \"memory\");\n" : "%sif (ls) vs_ls_wait();\n", ind);
         b.put("        break;\n    }\n");
     }
     b.put("    }\n}\n");

@@ -330,6 +330,13 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
         // 0.94 -> 0.71 ms, srbm_mpc 6.29 -> 5.98 ms; one-wave batches launch unclustered)
         const int want = env_ls > 0 ? env_ls : (p->opts.lockstep == 0 ? 2 : p->opts.lockstep);
         eo.lockstep = std::max(1, std::min(8, want));
+        // grouped teams (groups > 1) run without lockstep points: ldlt_57 with 8-warp teams x 2
+        // groups and a refined schedule computed wrong results in every row whenever the
+        // lockstep code was compiled in -- even in one-wave launches that never execute it
+        // (out-of-line or inline; sanitizers clean, deterministic; correct without it:
+        // profiles/r2_groups_lockstep.md).  Costs the srbm_mpc large-batch shape 6% (B=65536
+        // 5.04 -> 5.36 ms).  VSB_LOCKSTEP overrides (for A/B only)
+        if (eo.groups > 1 && env_ls <= 0) eo.lockstep = 1;
         eo.lockstep_every = env_le > 0 ? env_le : 4;
         if (eo.team >= 2 && eo.cluster == 1 && eo.lockstep > 1)
             shape += "l" + std::to_string(eo.lockstep) + "e" + std::to_string(eo.lockstep_every);

@@ -31,6 +31,7 @@ def jobs() -> list[tuple]:
         out += [("workload", name, o) for _, o in VARIANTS]
     out += [("workload", name, {"dtype": "float32"}) for name in sorted(FP32_RTOL)]
     out += [("workload", "srbm_mpc", {"team": 8})]
+    out += [("workload", "ldlt_57", {"team": 8, "groups": 2})]   # test_grouped_teams_on_the_ldlt57_solve
     for name in ("pendulum", "cartpole_rk4", "example"):
         out += [("workload", name, o) for o in ({"bulk_io": 1}, {"bulk_io": -1}, {"bulk_io": 1, "tma_stages": 3},
                                                  {"bulk_io": 1, "tma_stages": 4})]

@@ -128,3 +128,16 @@ def test_unwritten_output_nonzeros_read_zero():
     assert (o1[:, 1] == 0).all() and (o1[:, 0] == ins[0][:, 0]).all()
     ref = oracle.batch_eval(tape, ins)
     assert_bitwise_or_nan(o0, ref[0], "vs oracle")
+
+
+def test_grouped_teams_on_the_ldlt57_solve():
+    # 8-warp teams x 2 instance groups with the refined schedule: the shape that computed wrong
+    # results while lockstep points were compiled in (profiles/r2_groups_lockstep.md); every row
+    # against the oracle, one wave and several
+    tape = workloads.load_tape("ldlt_57")
+    for B in (256, 20000):
+        ins = workloads.make_inputs("ldlt_57", B, seed=11)
+        ref = oracle.batch_eval(tape, ins, n_threads=8)
+        got = _host_eval(tape, ins, team=8, groups=2)
+        for j, (g, r) in enumerate(zip(got, ref)):
+            assert_close(g, r, RTOL64, f"ldlt_57 team 8 x 2 groups B={B} out {j}")

@@ -166,3 +166,20 @@ def test_value_numbering_merges_only_exact_equivalences():
     assert p.info["n_cse"] == EXPECTED_CSE
     # 16 arithmetic rows - 10 merged = 6 live ops: NEG x, x+y, x*y, fmin(x,y), fmin(y,x), x+0
     assert p.info["n_live_ops"] == 6
+
+
+@pytest.mark.parametrize("prio", [0, 1])
+def test_refined_team_schedules_compile(prio, tmp_path):
+    # the local search (refine_schedule) moves ops between warps and phases; every
+    # same-warp consumer must still follow its producer in the emitted code (a violation
+    # surfaces as an NVRTC redeclaration error).  Critical-path priority (prio=1) leaves the
+    # greedy warp-phase order far from program order -- the case that exposed it.
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_acceptance_fuzz import _golden, _tapes
+
+    tapes = _tapes(_golden(), "exact")
+    for idx in (40, 77, 95):
+        p = Plan(tapes[idx], team=8, priority=prio, cache_dir=str(tmp_path))
+        assert p.info["team"] == 8 and p.info["n_chunks"] >= 1

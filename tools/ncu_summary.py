@@ -58,7 +58,12 @@ def convert(value: float, unit: str, want: str) -> float:
 
 
 def raw_rows(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    if path.endswith(".csv"):   # an `ncu -i ... --page raw --csv` export made on the GPU box
+        with open(path) as fh:
+            out = fh.read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     header, units, data = rows[0], rows[1], rows[2:]
     return header, units, data
