@@ -229,31 +229,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-# chip-wide instruction-fetch throughput for distinct per-warp code (straight-line DADD,
-# 16 warps/CTA, >=128 SMs busy): tools/ifetch_bench.py --scale, profiles/r1_ifetch_scale.jsonl
-IFETCH_PEAK = 1.04e11  # SASS instructions / s
+def issue_roof(workload, B, mean_s, clocks):
+    """Instruction-issue view of the team kernels.
 
-
-def ifetch_roof(plan, info, B, mean_s, clocks):
-    """Instruction-fetch roofline of the team kernels.
-
-    Each warp of a team CTA runs its own slice of straight-line code, so a CTA
-    fetches every instruction of its chunk kernels once per step: the work per
-    CTA is code_bytes/16 SASS instructions.  The chip streams distinct code
-    from L2 at IFETCH_PEAK instr/s (measured), whichever SMs fetch it.
-    achieved = instructions fetched by all CTAs / step time.
+    Warp-instructions executed per step come from the committed ncu capture of the same
+    plan (profiles/traffic.json <- r2_ncu_srbm_chunks_run11_raw.csv); divided by the live
+    step time they give the chip's issue rate, against 148 SMs x 4 schedulers x clock.  A
+    low fraction with low HBM and FP64 fractions is the signature of the binding limit: the
+    SM's instruction delivery to 16 distinct straight-line warp streams (~0.5-0.75
+    warp-instructions per cycle per busy SM, measured per phase in profiles/r2_phase_trace/).
     """
-    if not info.get("team") or info.get("code_bytes", 0) <= 0:
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            d = json.load(fh).get(workload)
+    except (OSError, ValueError):
         return None
-    ipb = 32 * max(1, info.get("groups", 1))
-    k = max(1, info.get("cluster", 1))
-    ctas = -(-B // ipb) * k            # runtime.cpp pick_ipc (VSB_IPC_FILL off)
-    instr = info["code_bytes"] / 16    # every CTA of a cluster-free team fetches its chunks' code once
-    achieved = instr * ctas / k / mean_s
-    return {"achieved": achieved, "peak": IFETCH_PEAK, "unit": "SASS instr/s (chip-wide fetch)",
-            "frac": achieved / IFETCH_PEAK, "code_instr_per_cta": instr / k, "ctas": ctas,
-            "peak_source": "tools/ifetch_bench.py --scale on B200: distinct straight-line code per warp, "
-                           "1.03-1.09e11 instr/s with 128-296 CTAs (profiles/r1_ifetch_scale.jsonl)"}
+    if not d or d.get("batch") != B or not d.get("warp_instr_per_step"):
+        return None
+    mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    achieved = d["warp_instr_per_step"] / mean_s
+    busy_sms = min(148, -(-B // 32))
+    return {"achieved": achieved, "peak": peak, "unit": "warp-instr/s", "frac": achieved / peak,
+            "ipc_per_busy_sm": achieved / (busy_sms * mhz * 1e6), "busy_sms": busy_sms,
+            "warp_instr_per_step": d["warp_instr_per_step"], "source": d["source"].split(":")[0]}
 
 
 def committed_traffic(workload, info, B):
@@ -551,7 +550,7 @@ def run_ours(args):
                "w1_value": rate1, "speedup_value_vs_cpu": value / rate, "speedup_e2e_vs_cpu": e2e_value / rate,
                "reference_numba": None if args.no_numba else reference_numba(tape, inputs, threads)}
 
-    ifetch = ifetch_roof(plan, info, B, mean_s, clocks)
+    issue = issue_roof(args.workload, B, mean_s, clocks) if info.get("team") else None
     secondary = sweep = None
     if world == 1 and not args.no_secondary:
         secondary = secondary_points(dev, local, hbm_gbs)
@@ -575,8 +574,9 @@ def run_ours(args):
                      "note": "achieved = algorithmic I/O bytes 8*(sum nnz_in + sum nnz_out) per eval x batch over"
                              " the whole kernel chain of one step (CUDA events); traffic = ncu dram bytes of the same"
                              " chain per step. Neither HBM nor the FP64 pipe binds a large tape at this batch: the"
-                             " binding roof is instruction fetch (see ifetch, DESIGN.md 4.4)",
-                     "ifetch": ifetch,
+                             " binding limit is instruction delivery to 16 distinct straight-line warp streams per SM"
+                             " (issue, DESIGN.md 4.4c)",
+                     "issue": issue,
                      "fp64": {"achieved": fp64_achieved, "peak": fp64_peak, "unit": "Tops/s",
                               "frac": fp64_achieved / fp64_peak,
                               "peak_def": "148 SM x 64 FP64 lanes x sm_max_mhz, 1 op/lane/clk (no FMA: --fmad=false)"}},
