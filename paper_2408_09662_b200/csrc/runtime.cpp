@@ -392,7 +392,19 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
 
 // the variant a call of n instances runs (AoS / SoA; the large-batch shape when eligible)
 int pick_variant(vsb_plan* p, int layout, int64_t n, Variant** out) {
-    if (p->wide_ok && n >= p->wide_min && (layout == VSB_AOS || layout == VSB_SOA)) layout |= kWideKey;
+    if (p->wide_ok && (layout == VSB_AOS || layout == VSB_SOA)) {
+        // whole waves decide: a wave of the grouped shape (64 instances per CTA) takes ~1.8x a
+        // wave of 16-warp teams (srbm_mpc: 0.72-0.77 vs 0.41 ms per wave), so it pays once it
+        // saves enough waves (B=10000: 3 vs 2 waves -> keep 16 warps; 16384: 4 vs 2 -> grouped)
+        bool wide;
+        if (p->wide_min > 0) {
+            wide = n >= p->wide_min;
+        } else {
+            const int64_t sms = 148, w16 = (n + sms * 32 - 1) / (sms * 32), w2 = (n + sms * 64 - 1) / (sms * 64);
+            wide = 10 * w16 > 18 * w2;
+        }
+        if (wide) layout |= kWideKey;
+    }
     return build_variant(p, layout, out);
 }
 
@@ -750,9 +762,9 @@ int vsb_plan_create(const int32_t* code, const double* values, int64_t n_rows, i
     if (team_auto && p->opts.team == 16 && p->opts.groups == 1 && p->opts.cluster == 1) {
         static const int64_t env_wide = getenv("VSB_WIDE_MIN") ? atoll(getenv("VSB_WIDE_MIN")) : -1;
         p->wide_ok = env_wide != 0;
-        // >= 2 waves of 16-warp team CTAs (srbm_mpc B=16384: 1.64 -> 1.44 ms, 65536: 6.04 -> 5.04;
-        // profiles/r2_sweeps_r09.jsonl)
-        p->wide_min = env_wide > 0 ? env_wide : 2 * 148 * 32;
+        // by wave count (pick_variant; srbm_mpc B=16384: 1.64 -> 1.44 ms, 65536: 6.04 -> 5.36;
+        // profiles/r2_sweeps_r09.jsonl, r2_14_sweep.jsonl); VSB_WIDE_MIN=n: a fixed threshold
+        p->wide_min = env_wide > 0 ? env_wide : 0;
     }
     int rc = build_variant(p.get(), VSB_AOS, &v);
     if (rc != VSB_OK) return rc;
