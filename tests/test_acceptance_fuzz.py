@@ -35,7 +35,8 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import GOLDEN, assert_bitwise_or_nan, assert_parity
+from conftest import GOLDEN, RTOL64, assert_bitwise_or_nan, assert_parity, close_mask
+from libm_replay import explained_by_libm
 from paper_2408_09662_b200 import BatchWorkspace, batch_eval, serial_eval
 from paper_2408_09662_b200.tape import deserialize
 
@@ -112,6 +113,7 @@ def test_acceptance_fuzz_gpu(fam):
     engaged = {"team": 0, "team_chunked": 0, "overflow": 0, "thread_chunked": 0}
     n_unstable, n_rows = [0], [0]
     failures = []
+    n_replayed = [0]
     for idx, tape in enumerate(tapes):
         master = inputs_for(fam, idx, tape.nnz_in, max(BATCHES))
         if fam == "acc":
@@ -137,6 +139,17 @@ def test_acceptance_fuzz_gpu(fam):
             n_unstable[0] += sum(int(u.sum()) for u in unstable)
             n_rows[0] += sum(u.size for u in unstable)
 
+        def _outside_rows(got, rows):
+            bad = set()
+            for j, g in enumerate(got):
+                r = ref[j][rows]
+                ok = close_mask(g, r, RTOL64)
+                with np.errstate(invalid="ignore"):
+                    ok |= np.isfinite(g) & np.isfinite(r) & (np.abs(g - r) <= 4.0 * np.asarray(spread[j][rows]))
+                ok |= unstable[j][rows]
+                bad.update(np.where(~ok.all(axis=1) if ok.ndim == 2 else ~ok)[0].tolist())
+            return sorted(bad)
+
         def check(got, what, rows=slice(None)):
             for j, g in enumerate(got):
                 r = ref[j][rows]
@@ -146,7 +159,17 @@ def test_acceptance_fuzz_gpu(fam):
                     else:
                         keep = ~unstable[j][rows]
                         assert_parity(g[keep], r[keep], spread[j][rows][keep], what=f"{what} out {j}")
-                except AssertionError as e:   # collected: every failing tape is reported
+                except AssertionError as e:
+                    # a kink flipped by the ulps libdevice returns, beyond what the 1-ulp
+                    # patterns predicted (acc57: ref NaN, GPU finite after a 1-ulp atan2
+                    # difference): accepted only if a CPU replay with the GPU's own
+                    # transcendental results -- each within 3 ulp of glibc -- reproduces the
+                    # GPU output bit for bit (tests/libm_replay.py)
+                    bad_rows = _outside_rows(got, rows)
+                    if spread is not None and 0 < len(bad_rows) <= 16 and explained_by_libm(
+                            tape, master, bad_rows, got, plan_options=opts or None):
+                        n_replayed[0] += len(bad_rows)
+                        continue
                     failures.append(str(e).splitlines()[0])
 
         for opts in [{}] + stress_options(tape, idx):
@@ -180,6 +203,7 @@ def test_acceptance_fuzz_gpu(fam):
                     for j, (a, b) in enumerate(zip(ser, full)):
                         assert_bitwise_or_nan(a, b[e], f"{what} serial_eval row {e} out {j}")
     assert not failures, "\n".join(failures)
+    assert n_replayed[0] <= 64, n_replayed[0]   # replay-explained rows stay rare
     # every regime was exercised; libm-unstable rows are rare
     assert n_unstable[0] <= 1e-3 * max(n_rows[0], 1), (n_unstable[0], n_rows[0])
     assert engaged["team"] >= 20 and engaged["team_chunked"] >= 10, engaged
