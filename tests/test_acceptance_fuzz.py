@@ -133,8 +133,9 @@ def test_acceptance_fuzz_gpu(fam):
         unstable = None
         if spread is not None:
             with np.errstate(invalid="ignore"):
-                # (a non-finite spread: some libm perturbation turned the value infinite / finite)
-                unstable = [~np.isfinite(np.asarray(sp)) | (np.asarray(sp) > 1e-6 * np.maximum(np.abs(r), 1.0))
+                # (an infinite spread: some libm perturbation turned an infinite value finite or
+                # back; a NaN spread is a value that stays NaN -- stable, compared NaN == NaN)
+                unstable = [np.isinf(np.asarray(sp)) | (np.asarray(sp) > 1e-6 * np.maximum(np.abs(r), 1.0))
                             for sp, r in zip(spread, ref)]
             n_unstable[0] += sum(int(u.sum()) for u in unstable)
             n_rows[0] += sum(u.size for u in unstable)
