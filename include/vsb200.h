@@ -29,9 +29,9 @@
 extern "C" {
 #endif
 
-#define VSB_ABI_VERSION 5   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
+#define VSB_ABI_VERSION 6   /* 2: vsb_options groups/cluster/outline/bulk_io, plan_info additions;
                                3: vsb_rollout_device, VSB_ERR_UNSUPPORTED; 4: vsb_options.flags/tma_stages/lockstep,
-                               vsb_plan_prepare_rollout; 5: vsb_plan_info.n_cse */
+                               vsb_plan_prepare_rollout; 5: vsb_plan_info.n_cse; 6: vsb_pipe_* */
 
 enum vsb_status {
     VSB_OK = 0,
@@ -190,6 +190,23 @@ int vsb_plan_prepare_rollout(vsb_plan *plan, int32_t state_in, int32_t state_out
  * Replaces: batchrt.batch_eval (batchrt.py:194-244) for one device. */
 int vsb_eval_host(vsb_plan *plan, const void *in_buf, const int64_t *in_off, void *out_buf,
                   const int64_t *out_off, int64_t e0, int64_t e1, int32_t device);
+
+/* Asynchronous host path for a stream of batches (a serving loop, a parameter sweep):
+ * vsb_pipe_submit enqueues what vsb_eval_host does for one batch -- pinned H2D, the
+ * kernel chain, D2H -- and returns without waiting, so batch k+1's input copy and
+ * batch k-1's output copy overlap batch k's kernels.  `depth` device workspaces
+ * rotate; a submission reusing a workspace waits (on the device) for its previous
+ * D2H.  The host buffers of a submission must stay untouched until vsb_pipe_wait
+ * returns for its ticket (or vsb_pipe_drain).  One pipe per host thread.
+ * Same layout and arguments as vsb_eval_host; no reference counterpart (the
+ * reference's batch_eval, batchrt.py:194-244, is synchronous). */
+typedef struct vsb_pipe vsb_pipe;
+int vsb_pipe_create(vsb_plan *plan, int32_t device, int32_t depth, vsb_pipe **pipe);
+int vsb_pipe_submit(vsb_pipe *pipe, const void *in_buf, const int64_t *in_off, void *out_buf,
+                    const int64_t *out_off, int64_t e0, int64_t e1, int64_t *ticket);
+int vsb_pipe_wait(vsb_pipe *pipe, int64_t ticket);
+int vsb_pipe_drain(vsb_pipe *pipe);
+int vsb_pipe_destroy(vsb_pipe *pipe);
 
 /* Batch sharder: split [e0, e1) into n_dev contiguous shards
  * (batchrt._chunk_bounds rule, batchrt.py:189-191) and run vsb_eval_host on

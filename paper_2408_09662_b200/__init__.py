@@ -7,7 +7,7 @@ executed by generated sm_100a kernels (NVRTC) behind the C ABI in
 ``include/vsb200.h``.  ``Function`` adds the torch tensor interface.
 """
 
-from .batchrt import BatchWorkspace, batch_eval, default_thread_count, serial_eval
+from .batchrt import BatchPipeline, BatchWorkspace, batch_eval, default_thread_count, serial_eval
 from .hoist import InvariantSplit, split_invariant
 from .plan import Plan, clear_plan_cache, get_plan
 from .tape import (
@@ -24,7 +24,7 @@ from .tape import (
 )
 
 __all__ = [
-    "BatchWorkspace", "batch_eval", "serial_eval", "default_thread_count",
+    "BatchWorkspace", "batch_eval", "serial_eval", "default_thread_count", "BatchPipeline",
     "Plan", "get_plan", "clear_plan_cache",
     "InstructionTape", "OpCode", "Sparsity", "arity", "as_tape", "deserialize", "serialize", "load", "save",
     "FORMAT_VERSION", "Function", "split_invariant", "InvariantSplit",

@@ -24,6 +24,7 @@ EXPORTS = (
     "vsb_eval_device_soa", "vsb_rollout_device", "vsb_plan_prepare_rollout",
     "vsb_eval_host", "vsb_eval_host_sharded", "vsb_transpose", "vsb_launches_per_eval",
     "vsb_host_alloc", "vsb_host_free", "vsb_debug_read_global",
+    "vsb_pipe_create", "vsb_pipe_submit", "vsb_pipe_wait", "vsb_pipe_drain", "vsb_pipe_destroy",
 )
 
 
@@ -153,6 +154,11 @@ def lib() -> ctypes.CDLL:
     L.vsb_host_alloc.argtypes = [ctypes.POINTER(vp), i64]
     L.vsb_host_free.argtypes = [vp]
     L.vsb_debug_read_global.argtypes = [vp, i32, ctypes.c_char_p, i32, vp, i64]
+    L.vsb_pipe_create.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    L.vsb_pipe_submit.argtypes = [vp, vp, i64p, vp, i64p, i64, i64, i64p]
+    L.vsb_pipe_wait.argtypes = [vp, i64]
+    L.vsb_pipe_drain.argtypes = [vp]
+    L.vsb_pipe_destroy.argtypes = [vp]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int:  # default restype: status code

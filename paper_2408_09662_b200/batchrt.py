@@ -27,7 +27,7 @@ from . import _native
 from .plan import get_plan
 from .tape import InstructionTape, as_tape
 
-__all__ = ["BatchWorkspace", "serial_eval", "batch_eval", "default_thread_count"]
+__all__ = ["BatchWorkspace", "serial_eval", "batch_eval", "default_thread_count", "BatchPipeline"]
 
 
 def default_thread_count() -> int:
@@ -162,6 +162,81 @@ def batch_eval(tape, ws: BatchWorkspace, n_threads: int | None = None, *, device
         dev = int(devices[0]) if devices else int(device)
         plan.eval_host(in_ptr, ws._in_off, out_ptr, ws._out_off, 0, ws.batch_size, dev)
     return ws.outputs
+
+
+class BatchPipeline:
+    """Asynchronous ``batch_eval`` over a stream of workspaces (``vsb_pipe_*``).
+
+    ``submit(ws)`` enqueues one batch -- pinned H2D, the kernel chain, D2H -- and
+    returns a ticket without waiting; ``wait(ticket)`` / ``drain()`` block until the
+    outputs are in ``ws.outputs``.  With ``depth`` batches in flight the next batch's
+    input copy and the previous batch's output copy overlap the current batch's
+    kernels, so a stream of batches costs max(H2D, kernels, D2H) per batch instead of
+    their sum.  A submitted workspace must not be modified or read until its ticket is
+    waited for.  Additive to the reference, whose ``batch_eval`` (batchrt.py:194-244)
+    is synchronous; results are the same bits as ``batch_eval``.
+    """
+
+    def __init__(self, tape, *, depth: int = 2, device: int = 0, plan_options: dict | None = None):
+        self.tape = as_tape(tape)
+        if not 1 <= int(depth) <= 16:
+            raise ValueError(f"depth must be in [1, 16], got {depth}")
+        self.device = int(device)
+        self._plan_options = plan_options
+        self._plan = None
+        self._h = None
+        self._depth = int(depth)
+        self._pending: dict[int, BatchWorkspace] = {}
+
+    def _open(self, ws: BatchWorkspace) -> None:
+        if self._h is not None:
+            return
+        self._plan = _plan_for(self.tape, ws, self._plan_options)
+        h = ctypes.c_void_p()
+        _native.check(_native.lib().vsb_pipe_create(self._plan.handle, self.device, self._depth, ctypes.byref(h)))
+        self._h = h
+        self._finalizer = weakref.finalize(self, _native.lib().vsb_pipe_destroy, h)
+
+    def submit(self, ws: BatchWorkspace) -> int:
+        if not ws.matches(self.tape):
+            raise ValueError(
+                f"workspace/tape mismatch: workspace is laid out for n_w={ws._n_w}, "
+                f"nnz_in={list(ws._nnz_in)}, nnz_out={list(ws._nnz_out)} but tape "
+                f"{self.tape.name!r} needs n_w={self.tape.n_w}, nnz_in={self.tape.nnz_in}, nnz_out={self.tape.nnz_out}"
+            )
+        self._open(ws)
+        ticket = ctypes.c_int64(-1)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        _native.check(_native.lib().vsb_pipe_submit(
+            self._h, ctypes.c_void_p(ws._in_buf.ctypes.data), ws._in_off.ctypes.data_as(i64p),
+            ctypes.c_void_p(ws._out_buf.ctypes.data), ws._out_off.ctypes.data_as(i64p),
+            0, ws.batch_size, ctypes.byref(ticket)))
+        self._pending[ticket.value] = ws   # keeps the host buffers alive while in flight
+        return ticket.value
+
+    def wait(self, ticket: int) -> list[np.ndarray]:
+        if ticket not in self._pending:
+            raise ValueError(f"unknown or already waited ticket {ticket}")
+        _native.check(_native.lib().vsb_pipe_wait(self._h, int(ticket)))
+        return self._pending.pop(ticket).outputs
+
+    def drain(self) -> None:
+        if self._h is not None:
+            _native.check(_native.lib().vsb_pipe_drain(self._h))
+        self._pending.clear()
+
+    def close(self) -> None:
+        if self._h is not None:
+            self._finalizer()
+            self._h = None
+        self._pending.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.drain()
+        self.close()
 
 
 def serial_eval(tape, input_values, *, device: int = 0) -> list[np.ndarray]:

@@ -596,6 +596,27 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
     pb[base] = reinterpret_cast<uint64_t>(scratch);
     int rc = VSB_OK;
+    // VSB_L2_PERSIST_MB=m (experiment): mark the chunk scratch as an L2 persisting access
+    // window (m MiB set aside for persisting lines) so that values crossing chunk boundaries
+    // are not evicted by register-spill traffic before the next chunk reads them
+    static const int64_t persist_env = getenv("VSB_L2_PERSIST_MB") ? atoll(getenv("VSB_L2_PERSIST_MB")) : 0;
+    int64_t persist_bytes = 0, persist_window = 0;
+    if (persist_env > 0 && scratch && v->ks.scratch_slots > 0) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        persist_bytes = std::min<int64_t>(persist_env << 20, max_persist);
+        persist_window = std::min<int64_t>(ld_max * v->ks.scratch_slots * p->rsz(), max_window);
+        static std::set<int> limit_set;
+        if (!limit_set.count(device)) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(persist_bytes));
+            limit_set.insert(device);
+            if (getenv("VSB_TRACE"))
+                fprintf(stderr, "[vsb trace] L2 persist %lld of max %d bytes, window %lld of max %d\n",
+                        (long long)persist_bytes, max_persist, (long long)persist_window, max_window);
+        }
+        if (persist_bytes <= 0 || persist_window <= 0) persist_bytes = 0;
+    }
     for (int64_t w0 = 0; w0 < n && rc == VSB_OK; w0 += wave) {
         const int64_t m = std::min(wave, n - w0);
         const int64_t ipc = pick_ipc(v->ks, m, n_sm);
@@ -613,22 +634,36 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             // then; a one-wave launch skips them, and with them their L1-invalidating acquire)
             const bool clustered = v->ks.lockstep > 1 && grid > n_sm;
             pb[base + 6] = clustered ? 1u : 0u;
+            cudaLaunchAttribute attr[2];
+            unsigned na = 0;
             if (clustered) {
                 // several waves: pairs (lockstep) of CTAs share a cluster and meet at a relaxed
                 // cluster barrier every few phases -- their identical instruction streams stay
                 // together (humanoid_rbd B=65536: 0.94 -> 0.71 ms, profiles/r2_summary.md)
+                attr[na].id = cudaLaunchAttributeClusterDimension;
+                attr[na].val.clusterDim.x = static_cast<unsigned>(v->ks.lockstep);
+                attr[na].val.clusterDim.y = 1;
+                attr[na].val.clusterDim.z = 1;
+                ++na;
+            }
+            if (persist_bytes > 0) {
+                attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+                attr[na].val.accessPolicyWindow.base_ptr = scratch;
+                attr[na].val.accessPolicyWindow.num_bytes = static_cast<size_t>(persist_window);
+                attr[na].val.accessPolicyWindow.hitRatio =
+                    static_cast<float>(std::min(1.0, static_cast<double>(persist_bytes) / static_cast<double>(persist_window)));
+                attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                ++na;
+            }
+            if (na) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(static_cast<unsigned>(grid));
                 cfg.blockDim = dim3(ch.threads);
                 cfg.dynamicSmemBytes = static_cast<size_t>(ch.smem_bytes);
                 cfg.stream = stream;
-                cudaLaunchAttribute attr[1];
-                attr[0].id = cudaLaunchAttributeClusterDimension;
-                attr[0].val.clusterDim.x = static_cast<unsigned>(v->ks.lockstep);
-                attr[0].val.clusterDim.y = 1;
-                attr[0].val.clusterDim.z = 1;
                 cfg.attrs = attr;
-                cfg.numAttrs = 1;
+                cfg.numAttrs = na;
                 e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(v->kerns[c]), args);
             } else {
                 e = cudaLaunchKernel(reinterpret_cast<const void*>(v->kerns[c]), dim3(static_cast<unsigned>(grid)),
@@ -1218,6 +1253,182 @@ int vsb_eval_host(vsb_plan* p, const void* in_buf, const int64_t* in_off, void* 
     }
     if (rc != VSB_OK) return rc;
     if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("eval_host: ") + cudaGetErrorString(e));
+    return VSB_OK;
+}
+
+// ---- asynchronous host path over a stream of batches (vsb_pipe_*) ---------------------
+// Three engines run at once: the H2D copy engine, the SMs and the D2H copy engine.  A
+// synchronous call (vsb_eval_host) uses them one after the other for a latency-bound team
+// chain (srbm_mpc B=4096: H2D 0.15 + kernels 0.40 + D2H 0.13 ms); a pipe keeps `depth`
+// batches in flight so that, in steady state, a batch costs max(H2D, kernels, D2H).
+struct vsb_pipe {
+    vsb_plan* p = nullptr;
+    int device = 0;
+    struct Slot {
+        void* base = nullptr;     // inputs | outputs | chain scratch of one batch
+        size_t bytes = 0;
+        cudaStream_t sc = nullptr;  // this slot's kernel chain
+        cudaEvent_t in_done = nullptr, k_done = nullptr, out_done = nullptr;
+        int64_t ticket = -1;        // newest submission that used the slot
+    };
+    std::vector<Slot> slots;
+    cudaStream_t sh = nullptr, sd = nullptr;  // all H2D copies / all D2H copies, in submission order
+    int64_t next = 0;
+};
+
+static void pipe_release(vsb_pipe* q) {
+    if (!q) return;
+    DeviceGuard g(q->device);
+    if (q->sd) cudaStreamSynchronize(q->sd);
+    for (auto& s : q->slots) {
+        if (s.sc) { cudaStreamSynchronize(s.sc); cudaStreamDestroy(s.sc); }
+        for (cudaEvent_t e : {s.in_done, s.k_done, s.out_done}) if (e) cudaEventDestroy(e);
+        if (s.base) cudaFree(s.base);
+    }
+    if (q->sh) cudaStreamDestroy(q->sh);
+    if (q->sd) cudaStreamDestroy(q->sd);
+    delete q;
+}
+
+int vsb_pipe_create(vsb_plan* p, int32_t device, int32_t depth, vsb_pipe** out) {
+    if (!p || !out) return fail(VSB_ERR_INVALID, "null plan or pipe pointer");
+    *out = nullptr;
+    if (depth < 1 || depth > 16) return fail(VSB_ERR_INVALID, "pipe depth must be in [1, 16]");
+    DEVICE_GUARD(device);
+    vsb_pipe* q = new vsb_pipe;
+    q->p = p;
+    q->device = device;
+    q->slots.resize(static_cast<size_t>(depth));
+    cudaError_t e = cudaStreamCreateWithFlags(&q->sh, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q->sd, cudaStreamNonBlocking);
+    for (auto& s : q->slots) {
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s.sc, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.in_done, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.k_done, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.out_done, cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        pipe_release(q);
+        return fail(VSB_ERR_CUDA, std::string("vsb_pipe_create: ") + cudaGetErrorString(e));
+    }
+    *out = q;
+    return VSB_OK;
+}
+
+int vsb_pipe_submit(vsb_pipe* q, const void* in_buf, const int64_t* in_off, void* out_buf, const int64_t* out_off,
+                    int64_t e0, int64_t e1, int64_t* ticket) {
+    if (!q) return fail(VSB_ERR_INVALID, "null pipe");
+    vsb_plan* p = q->p;
+    int rc = check_range(p, e0, e1);
+    if (rc != VSB_OK) return rc;
+    const int n_in = static_cast<int>(p->prog.nnz_in.size()), n_out = static_cast<int>(p->prog.nnz_out.size());
+    if ((n_in && (!in_buf || !in_off)) || (n_out && (!out_buf || !out_off))) return fail(VSB_ERR_INVALID, "null buffer");
+    const int device = q->device;
+    DEVICE_GUARD(device);
+    const int64_t n = e1 - e0;
+    Variant* v = nullptr;
+    if (n > 0) {
+        std::lock_guard<std::mutex> lk(p->mu);
+        rc = pick_variant(p, VSB_AOS, n, &v);
+        if (rc == VSB_OK) rc = ensure_loaded(v, device);
+        if (rc != VSB_OK) return rc;
+        ensure_pool(p, device);
+    }
+    const int64_t t = q->next++;
+    if (ticket) *ticket = t;
+    if (n == 0) return VSB_OK;
+    auto& s = q->slots[static_cast<size_t>(t % static_cast<int64_t>(q->slots.size()))];
+    const int rs = p->rsz();
+    auto align = [](int64_t b) { return (b + 255) / 256 * 256; };
+    std::vector<int64_t> off_in(n_in), off_out(n_out);
+    int64_t total = 0;
+    for (int i = 0; i < n_in; ++i) { off_in[i] = total; total += n * p->prog.nnz_in[i] * rs; }
+    total = align(total);
+    for (int j = 0; j < n_out; ++j) { off_out[j] = total; total += n * p->prog.nnz_out[j] * rs; }
+    total = align(total);
+    const int64_t off_scr = total;
+    total += align(chain_scratch_bytes(p, v, n, sm_count(device)));
+    if (s.bytes < static_cast<size_t>(total)) {
+        // grow: the slot's previous batch must be finished with the old buffer
+        if (s.ticket >= 0) CUDA_TRY(cudaEventSynchronize(s.out_done));
+        if (s.base) CUDA_TRY(cudaFree(s.base));
+        s.base = nullptr;
+        s.bytes = 0;
+        CUDA_TRY(cudaMalloc(&s.base, static_cast<size_t>(std::max<int64_t>(total, 256))));
+        s.bytes = static_cast<size_t>(std::max<int64_t>(total, 256));
+    }
+    char* wb = static_cast<char*>(s.base);
+    // the slot's inputs are overwritten only after its previous batch left the device
+    if (s.ticket >= 0) cudaStreamWaitEvent(q->sh, s.out_done, 0);
+    const char* hin = static_cast<const char*>(in_buf);
+    char* hout = static_cast<char*>(out_buf);
+    auto contiguous = [&](const int64_t* off, const std::vector<int64_t>& nnz) {
+        for (size_t i = 0; i + 1 < nnz.size(); ++i)
+            if (off[i] + (e0 + n) * nnz[i] != off[i + 1] + e0 * nnz[i + 1]) return false;
+        return true;
+    };
+    cudaError_t e = cudaSuccess;
+    if (n_in > 0 && contiguous(in_off, p->prog.nnz_in)) {
+        if (p->prog.in_base[n_in] > 0)
+            e = cudaMemcpyAsync(wb + off_in[0], hin + (in_off[0] + e0 * p->prog.nnz_in[0]) * rs,
+                                static_cast<size_t>(n * p->prog.in_base[n_in] * rs), cudaMemcpyHostToDevice, q->sh);
+    } else {
+        for (int i = 0; i < n_in && e == cudaSuccess; ++i)
+            if (p->prog.nnz_in[i])
+                e = cudaMemcpyAsync(wb + off_in[i], hin + (in_off[i] + e0 * p->prog.nnz_in[i]) * rs,
+                                    static_cast<size_t>(n * p->prog.nnz_in[i] * rs), cudaMemcpyHostToDevice, q->sh);
+    }
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("pipe H2D: ") + cudaGetErrorString(e));
+    cudaEventRecord(s.in_done, q->sh);
+    cudaStreamWaitEvent(s.sc, s.in_done, 0);
+    std::vector<const void*> ins(n_in, nullptr);
+    std::vector<void*> outs(n_out, nullptr);
+    for (int i = 0; i < n_in; ++i) if (p->prog.nnz_in[i]) ins[i] = wb + off_in[i];
+    for (int j = 0; j < n_out; ++j) if (p->prog.nnz_out[j]) outs[j] = wb + off_out[j];
+    rc = launch_chain(p, v, ins, outs, 0, n, 0, s.sc, device, v->ks.scratch_slots > 0 ? wb + off_scr : nullptr);
+    if (rc != VSB_OK) return rc;
+    cudaEventRecord(s.k_done, s.sc);
+    cudaStreamWaitEvent(q->sd, s.k_done, 0);
+    if (n_out > 0 && contiguous(out_off, p->prog.nnz_out)) {
+        if (p->prog.out_base[n_out] > 0)
+            e = cudaMemcpyAsync(hout + (out_off[0] + e0 * p->prog.nnz_out[0]) * rs, wb + off_out[0],
+                                static_cast<size_t>(n * p->prog.out_base[n_out] * rs), cudaMemcpyDeviceToHost, q->sd);
+    } else {
+        for (int j = 0; j < n_out && e == cudaSuccess; ++j)
+            if (p->prog.nnz_out[j])
+                e = cudaMemcpyAsync(hout + (out_off[j] + e0 * p->prog.nnz_out[j]) * rs, wb + off_out[j],
+                                    static_cast<size_t>(n * p->prog.nnz_out[j] * rs), cudaMemcpyDeviceToHost, q->sd);
+    }
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("pipe D2H: ") + cudaGetErrorString(e));
+    cudaEventRecord(s.out_done, q->sd);
+    s.ticket = t;
+    return VSB_OK;
+}
+
+int vsb_pipe_wait(vsb_pipe* q, int64_t ticket) {
+    if (!q) return fail(VSB_ERR_INVALID, "null pipe");
+    if (ticket < 0 || ticket >= q->next) return fail(VSB_ERR_INVALID, "unknown pipe ticket");
+    const auto& s = q->slots[static_cast<size_t>(ticket % static_cast<int64_t>(q->slots.size()))];
+    // a newer batch on the same slot completes after this one (its H2D waited for our D2H)
+    if (s.ticket < ticket) return VSB_OK;   // an empty batch: nothing was enqueued
+    DEVICE_GUARD(q->device);
+    cudaError_t e = cudaEventSynchronize(s.out_done);
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("vsb_pipe_wait: ") + cudaGetErrorString(e));
+    return VSB_OK;
+}
+
+int vsb_pipe_drain(vsb_pipe* q) {
+    if (!q) return fail(VSB_ERR_INVALID, "null pipe");
+    DEVICE_GUARD(q->device);
+    cudaError_t e = cudaStreamSynchronize(q->sd);
+    for (auto& s : q->slots)
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s.sc);
+    if (e != cudaSuccess) return fail(VSB_ERR_CUDA, std::string("vsb_pipe_drain: ") + cudaGetErrorString(e));
+    return VSB_OK;
+}
+
+int vsb_pipe_destroy(vsb_pipe* q) {
+    pipe_release(q);
     return VSB_OK;
 }
 

@@ -141,3 +141,35 @@ def test_grouped_teams_on_the_ldlt57_solve():
         got = _host_eval(tape, ins, team=8, groups=2)
         for j, (g, r) in enumerate(zip(got, ref)):
             assert_close(g, r, RTOL64, f"ldlt_57 team 8 x 2 groups B={B} out {j}")
+
+
+@pytest.mark.parametrize("name, sizes, depth", [
+    ("srbm_mpc", (4096, 4096, 1000, 4096, 37), 2),     # team chain; a smaller batch reuses a grown slot
+    ("srbm_mpc", (4096,) * 4, 3),
+    ("cartpole_rk4", (100_000, 7, 65_536, 1), 2),      # thread mode (TMA tiles, tails)
+    ("humanoid_rbd", (4096, 8192, 4096), 1),           # depth 1: every batch reuses the one slot
+])
+def test_pipeline_matches_batch_eval_bitwise(name, sizes, depth):
+    """BatchPipeline (vsb_pipe_*) with several batches in flight returns the same bits as
+    the synchronous batch_eval of each workspace, and the oracle's values."""
+    from paper_2408_09662_b200 import BatchPipeline
+
+    tape = workloads.load_tape(name)
+    wss, want = [], []
+    for k, B in enumerate(sizes):
+        ins = workloads.make_inputs(name, B, seed=400 + k)
+        ws = BatchWorkspace(tape, B)
+        for i, v in enumerate(ins):
+            ws.set_input(i, v)
+        wss.append((ws, ins))
+        want.append(_host_eval(tape, ins))
+    with BatchPipeline(tape, depth=depth) as pipe:
+        tickets = [pipe.submit(ws) for ws, _ in wss]
+        for t, (ws, ins), ref in zip(tickets, wss, want):
+            got = pipe.wait(t)
+            for j, (g, r) in enumerate(zip(got, ref)):
+                assert_bitwise_or_nan(g.reshape(r.shape), r, f"{name} pipe depth {depth} B={ws.batch_size} out {j}")
+    ws, ins = wss[0]
+    ref = oracle.batch_eval(tape, [v[:256] for v in ins], n_threads=8)
+    for j, r in enumerate(ref):
+        assert_close(ws.output_matrix(j)[:256], r, RTOL64, f"{name} pipe vs oracle out {j}")

@@ -183,3 +183,33 @@ def test_refined_team_schedules_compile(prio, tmp_path):
     for idx in (40, 77, 95):
         p = Plan(tapes[idx], team=8, priority=prio, cache_dir=str(tmp_path))
         assert p.info["team"] == 8 and p.info["n_chunks"] >= 1
+
+
+def test_pipeline_argument_errors_without_gpu():
+    """BatchPipeline / vsb_pipe_* reject bad arguments before touching a device."""
+    import ctypes
+
+    from paper_2408_09662_b200 import BatchPipeline, _native
+
+    t = workloads.load_tape("pendulum")
+    with pytest.raises(ValueError, match="depth must be in"):
+        BatchPipeline(t, depth=0)
+    pipe = BatchPipeline(t)
+    with pytest.raises(ValueError, match="workspace/tape mismatch"):
+        pipe.submit(BatchWorkspace(workloads.load_tape("example"), 3))
+    with pytest.raises(ValueError, match="unknown or already waited ticket"):
+        pipe.wait(0)
+    L = _native.lib()
+    h = ctypes.c_void_p()
+    with pytest.raises(ValueError, match="depth"):
+        _native.check(L.vsb_pipe_create(vsb_plan_handle(t), 0, 0, ctypes.byref(h)))
+    for rc in (L.vsb_pipe_submit(None, None, None, None, None, 0, 1, None), L.vsb_pipe_wait(None, 0),
+               L.vsb_pipe_drain(None)):
+        with pytest.raises(ValueError, match="null pipe"):
+            _native.check(rc)
+
+
+def vsb_plan_handle(tape):
+    from paper_2408_09662_b200 import get_plan
+
+    return get_plan(tape).handle
