@@ -1961,52 +1961,6 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     // reaches each phase barrier and when it leaves it; read back with vsb_debug_read_global
     static const bool ptrace = getenv("VSB_PHASE_TRACE") && atoi(getenv("VSB_PHASE_TRACE")) != 0;
     if (ptrace) b.put("__device__ unsigned long long vs_ptrace[%lld];\n", (long long)(2 * W * P + W));
-    // VSB_SPREFETCH=D (experiment): at the start of phase ph every warp prefetches into L2 the
-    // chunk-scratch rows (values imported from earlier chunks, cross-warp overflow slots) that
-    // its phase ph+D reads (phases 0..D at kernel start), so their loads hit L2 instead of DRAM
-    // (ncu: c2/c4 read 55-61 MB from DRAM at a 60-72% L2 hit rate).  The slot lists live in a
-    // table (vs_pft); lane i issues one 256-byte bulk L2 prefetch (the row of VS_IPB = 32
-    // instances) per 32 entries, so the straight-line stream carries a few instructions per
-    // phase, not one prefetch per value.
-    static const int pf_env = getenv("VSB_SPREFETCH") ? atoi(getenv("VSB_SPREFETCH")) : 0;
-    const int pfd = (pf_env > 0 && IPB == 32 && K == 1 && !f32 && !soa) ? pf_env : 0;
-    std::vector<std::vector<std::pair<int64_t, int64_t>>> pf_at(pfd ? W : 0, std::vector<std::pair<int64_t, int64_t>>(P));
-    if (pfd) {
-        std::vector<int32_t> pft;
-        for (int w = 0; w < W; ++w)
-            for (int ph = 0; ph < P; ++ph) {
-                const int lo = ph == 0 ? 0 : ph + pfd, hi = ph == 0 ? pfd + 1 : ph + pfd + 1;
-                std::vector<int32_t> slots;
-                for (int r = lo; r < std::min(hi, P); ++r)
-                    for (int32_t q : ts.seq[w][r]) {
-                        const Node& nd = p.nodes[q];
-                        for (int k = 0; k < kArity[nd.op]; ++k) {
-                            const int32_t u = nd.arg[k];
-                            const int op = p.nodes[u].op;
-                            if (op == OP_CONST || op == OP_INPUT) continue;
-                            if (!in_chunk(u)) { if (slot_of[u] >= 0) slots.push_back(slot_of[u]); }
-                            else if (warp_of[u] != w && to_global[u]) slots.push_back(static_cast<int32_t>(cross_slots + xslot[u]));
-                        }
-                    }
-                std::sort(slots.begin(), slots.end());
-                slots.erase(std::unique(slots.begin(), slots.end()), slots.end());
-                pf_at[w][ph] = {static_cast<int64_t>(pft.size()), static_cast<int64_t>(slots.size())};
-                pft.insert(pft.end(), slots.begin(), slots.end());
-            }
-        b.put("__device__ const int vs_pft[%lld] = {", (long long)std::max<size_t>(pft.size(), 1));
-        for (size_t i = 0; i < pft.size(); ++i) b.put(i % 24 ? "%d," : "\n%d,", pft[i]);
-        if (pft.empty()) b.put("0");
-        b.put("};\n");
-        b.put("#define vs_pf_l2(off) asm volatile(\"cp.async.bulk.prefetch.L2.global [%%0], 256;\" :: "
-              "\"l\"(Sb + (long long)__ldg(vs_pft + (off) + lane) * VS_IPB) : \"memory\")\n");
-    }
-    auto emit_prefetch = [&](int w, int ph, const char* ind) {
-        if (!pfd) return;
-        const int64_t off = pf_at[w][ph].first, cnt = pf_at[w][ph].second;
-        for (int64_t j = 0; j < cnt; j += 32)
-            b.put(cnt - j >= 32 ? "%svs_pf_l2(%lld);\n" : "%sif (lane < %lld) vs_pf_l2(%lld);\n", ind,
-                  cnt - j >= 32 ? (long long)(off + j) : (long long)(cnt - j), (long long)(off + j));
-    };
     if (K > 1)
         b.put("extern \"C\" __global__ void __cluster_dims__(%d, 1, 1) __launch_bounds__(VS_BS, %d) %s(const VsArgs A) {\n",
               K, opt.min_blocks, nbuf);
@@ -2038,7 +1992,6 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     b.put("    real* __restrict__ X = vs_smem + grp * 32 + lane;\n");
     b.put("    real* __restrict__ X2 = vs_smem + (grp * 32 + lane) * 2;   // paired rows [row][lane][2]\n");
     b.put("    (void)S; (void)X; (void)X2;\n");
-    if (pfd) b.put("    const real* Sb = A.scratch + cid * (VS_NSLOT * VS_IPB) + grp * 32;\n");
     if (K > 1) {
         // shared::cluster addresses of this lane's X column in every CTA of the cluster
         b.put("    const unsigned xl = (unsigned)__cvta_generic_to_shared(X);\n");
@@ -2079,7 +2032,6 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
     for (int w = 0; w < W; ++w) {
         b.put("    case %d: {\n", w);
         const char* ind = "        ";
-        emit_prefetch(w, 0, ind);
         auto ensure = [&](int32_t u) {
             const Node& nu = p.nodes[u];
             if (nu.op == OP_CONST) return;
@@ -2124,7 +2076,6 @@ void Emitter::team_kernel_source(TeamPlan& tp, int c, Chunk& ch, Out& b) {
             emit_store(b, s, opnd(u), ind, false);
         }
         for (int ph = 0; ph < P; ++ph) {
-            if (ph > 0) emit_prefetch(w, ph, ind);
             for (int32_t q : ts.seq[w][ph]) {
                 const Node& nd = p.nodes[q];
                 if (sync_at[q] >= 0) b.put("%sVS_BSYNC(%d);\n", ind, 1 + sync_at[q] % 15);

@@ -596,27 +596,6 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
     const size_t base = static_cast<size_t>(std::max(n_in, 1) + std::max(n_out, 1));
     pb[base] = reinterpret_cast<uint64_t>(scratch);
     int rc = VSB_OK;
-    // VSB_L2_PERSIST_MB=m (experiment): mark the chunk scratch as an L2 persisting access
-    // window (m MiB set aside for persisting lines) so that values crossing chunk boundaries
-    // are not evicted by register-spill traffic before the next chunk reads them
-    static const int64_t persist_env = getenv("VSB_L2_PERSIST_MB") ? atoll(getenv("VSB_L2_PERSIST_MB")) : 0;
-    int64_t persist_bytes = 0, persist_window = 0;
-    if (persist_env > 0 && scratch && v->ks.scratch_slots > 0) {
-        int max_persist = 0, max_window = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
-        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
-        persist_bytes = std::min<int64_t>(persist_env << 20, max_persist);
-        persist_window = std::min<int64_t>(ld_max * v->ks.scratch_slots * p->rsz(), max_window);
-        static std::set<int> limit_set;
-        if (!limit_set.count(device)) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(persist_bytes));
-            limit_set.insert(device);
-            if (getenv("VSB_TRACE"))
-                fprintf(stderr, "[vsb trace] L2 persist %lld of max %d bytes, window %lld of max %d\n",
-                        (long long)persist_bytes, max_persist, (long long)persist_window, max_window);
-        }
-        if (persist_bytes <= 0 || persist_window <= 0) persist_bytes = 0;
-    }
     for (int64_t w0 = 0; w0 < n && rc == VSB_OK; w0 += wave) {
         const int64_t m = std::min(wave, n - w0);
         const int64_t ipc = pick_ipc(v->ks, m, n_sm);
@@ -634,7 +613,7 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
             // then; a one-wave launch skips them, and with them their L1-invalidating acquire)
             const bool clustered = v->ks.lockstep > 1 && grid > n_sm;
             pb[base + 6] = clustered ? 1u : 0u;
-            cudaLaunchAttribute attr[2];
+            cudaLaunchAttribute attr[1];
             unsigned na = 0;
             if (clustered) {
                 // several waves: pairs (lockstep) of CTAs share a cluster and meet at a relaxed
@@ -644,16 +623,6 @@ int launch_chain(vsb_plan* p, Variant* v, const std::vector<const void*>& ins, c
                 attr[na].val.clusterDim.x = static_cast<unsigned>(v->ks.lockstep);
                 attr[na].val.clusterDim.y = 1;
                 attr[na].val.clusterDim.z = 1;
-                ++na;
-            }
-            if (persist_bytes > 0) {
-                attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
-                attr[na].val.accessPolicyWindow.base_ptr = scratch;
-                attr[na].val.accessPolicyWindow.num_bytes = static_cast<size_t>(persist_window);
-                attr[na].val.accessPolicyWindow.hitRatio =
-                    static_cast<float>(std::min(1.0, static_cast<double>(persist_bytes) / static_cast<double>(persist_window)));
-                attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-                attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
                 ++na;
             }
             if (na) {
