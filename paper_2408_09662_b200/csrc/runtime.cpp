@@ -297,6 +297,13 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
         eo.team = 8;
         eo.groups = 2;
         eo.remat_gap = 256;
+    } else if (eo.team >= 2 && p->prog.n_live_ops >= 40000) {
+        // large team tapes: reload inputs / chunk imports idle for > 128 of the warp's ops
+        // instead of holding them in registers (fewer spills): srbm_mpc B=4096 0.434 -> 0.408 ms,
+        // rbd_chain12 0.574 -> 0.506, ldlt_57 0.370 -> 0.341; smaller team tapes gain nothing
+        // (humanoid_rbd B=65536 0.666 -> 0.694; profiles/r2_sweeps_r21_remat_srbm.jsonl,
+        // r2_sweeps_r22_remat_team.jsonl)
+        eo.remat_gap = 128;
     }
     eo.bulk_io = p->opts.bulk_io >= 0 && !roll;
     // outlined subroutines (bit 0 DIV, bit 1 SIN/COS, bit 2 EXP/LOG/POW/TAN/ATAN2): team kernels

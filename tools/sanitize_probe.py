@@ -24,8 +24,9 @@ import oracle  # noqa: E402
 from paper_2408_09662_b200 import Function  # noqa: E402
 
 args = sys.argv[1:]
-host = "--host" in args   # through batch_eval (the host path: streamed H2D inputs for team plans)
-args = [a for a in args if a != "--host"]
+host = "--host" in args   # through batch_eval (the synchronous host path)
+pipe = "--pipe" in args   # through BatchPipeline (3 batches, depth 2: slot reuse, overlapping copies)
+args = [a for a in args if a not in ("--host", "--pipe")]
 if args[0] == "--fuzz":
     from test_acceptance_fuzz import _golden, _tapes, inputs_for
 
@@ -41,7 +42,24 @@ else:
     ins = workloads.make_inputs(name, B, seed=5)
     opts = json.loads(args[2]) if len(args) > 2 else {}
 f = Function(tape, **opts)
-if host:
+if pipe:
+    from paper_2408_09662_b200 import BatchPipeline, BatchWorkspace
+
+    wss = []
+    for k in range(3):
+        ws = BatchWorkspace(tape, B)
+        for i, v in enumerate(ins):
+            ws.set_input(i, v)
+        wss.append(ws)
+    with BatchPipeline(tape, depth=2, plan_options=opts or None) as p:
+        tickets = [p.submit(ws) for ws in wss]
+        for t in tickets:
+            p.wait(t)
+    for ws in wss[1:]:
+        assert all(np.array_equal(ws.output_matrix(j), wss[0].output_matrix(j), equal_nan=True)
+                   for j in range(tape.n_out))
+    outs = [torch.tensor(wss[-1].output_matrix(j).copy()) for j in range(tape.n_out)]
+elif host:
     from paper_2408_09662_b200 import BatchWorkspace, batch_eval
 
     ws = BatchWorkspace(tape, B)
@@ -61,6 +79,6 @@ for o, r in zip(outs, ref):
     e[np.isnan(g) & np.isnan(r)] = 0
     worst = max(worst, float(np.nanmax(e)) if e.size else 0.0)
 info = f.plan.info
-print(json.dumps({"tape": tape.name, "batch": B, "opts": opts, "host": host, "team": info["team"], "chunks": info["n_chunks"],
+print(json.dumps({"tape": tape.name, "batch": B, "opts": opts, "host": host, "pipe": pipe, "team": info["team"], "chunks": info["n_chunks"],
                   "overflow_slots": info["overflow_slots"], "max_rel_err": worst}))
 sys.exit(0 if worst <= 1e-9 else 1)
