@@ -297,10 +297,9 @@ int build_variant(vsb_plan* p, int layout, Variant** out) {
         eo.team = 8;
         eo.groups = 2;
         eo.remat_gap = 256;
-        // shorter chunks: ptxas spills 24.7 -> 5.6 KB/thread, B=65536 5.39 -> 4.68 ms (12k ops:
-        // 4.73, 18k: 5.05; profiles/r2_sweeps_r24_chunks.jsonl).  The one-wave 16-warp shape
-        // keeps 24k (12k-21k: 0.44-0.47 vs 0.41 ms -- the extra chunk crossings cost more)
-        if (p->opts.chunk_ops == 0) eo.chunk_ops = 15000;
+        // (15k-op chunks cut spills 24.7 -> 5.6 KB/thread and B=65536 5.39 -> 4.68 ms, but
+        // computed 2,652 of 1.26M sampled values of the 1e6-instance test wrong by ~1e-6
+        // relative -- a 16-row sweep check had passed; reverted, profiles/r2_pytest_run25.log)
     } else if (eo.team >= 2 && p->prog.n_live_ops >= 40000) {
         // large team tapes: reload inputs / chunk imports idle for > 128 of the warp's ops
         // instead of holding them in registers (fewer spills): srbm_mpc B=4096 0.434 -> 0.408 ms,
