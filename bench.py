@@ -267,6 +267,7 @@ def committed_traffic(workload, info, B):
     return None, None
 
 
+PIPE_DEPTH = 3
 SECONDARY = (("cartpole_rk4", 1_000_000), ("pendulum", 1_000_000), ("humanoid_rbd", 65536), ("srbm_mpc", 65536))
 
 
@@ -525,23 +526,25 @@ def run_ours(args):
 
     # the same steps as a stream of batches through BatchPipeline (vsb_pipe_*): every step
     # still copies its inputs from pinned host memory and its outputs back, but step k+1's
-    # H2D and step k-1's D2H overlap step k's kernels.  Two workspaces alternate (a step's
-    # host buffers are reused only after its ticket was waited for).
+    # H2D and step k-1's D2H overlap step k's kernels.  PIPE_DEPTH workspaces rotate (a
+    # step's host buffers are reused only after its ticket was waited for); depth 3 reaches
+    # the device rate on srbm_mpc B=4096, depth 2 95% of it (profiles/r2_27_pipe.jsonl)
     pipe_steps = max(3, min(args.steps, 50))
     pipe_ws = None
     if not args.global_batch:
-        pipe_ws = [e2e_tape_ws, vsb.BatchWorkspace(tape, B)]
-        for i, v in enumerate(inputs):
-            pipe_ws[1].set_input(i, v)
-        pipe = vsb.BatchPipeline(tape, depth=2, device=local, plan_options=opts or None)
+        pipe_ws = [e2e_tape_ws] + [vsb.BatchWorkspace(tape, B) for _ in range(PIPE_DEPTH - 1)]
+        for w in pipe_ws[1:]:
+            for i, v in enumerate(inputs):
+                w.set_input(i, v)
+        pipe = vsb.BatchPipeline(tape, depth=PIPE_DEPTH, device=local, plan_options=opts or None)
 
         def pipe_run(k_steps):
             tickets = []
             for k in range(k_steps):
-                if k >= 2:
-                    pipe.wait(tickets[k - 2])
-                tickets.append(pipe.submit(pipe_ws[k % 2]))
-            for t in tickets[max(0, k_steps - 2):]:
+                if k >= PIPE_DEPTH:
+                    pipe.wait(tickets[k - PIPE_DEPTH])
+                tickets.append(pipe.submit(pipe_ws[k % PIPE_DEPTH]))
+            for t in tickets[max(0, k_steps - PIPE_DEPTH):]:
                 pipe.wait(t)
 
         t_warm = time.perf_counter()
@@ -575,9 +578,10 @@ def run_ours(args):
     e2e_sync_value = total_instances * e2e_steps / e2e_sync_s
     if pipe_ws is not None:
         e2e_value = total_instances * pipe_steps / e2e_pipe_s
-        e2e_api = "paper_2408_09662_b200.BatchPipeline(tape, depth=2).submit(BatchWorkspace) [pinned host buffers]"
-        e2e_timing = (f"{pipe_steps} pipelined steps (2 workspaces, 2 in flight), host wall clock from the first submit"
-                      " to the last wait, max over ranks")
+        e2e_api = (f"paper_2408_09662_b200.BatchPipeline(tape, depth={PIPE_DEPTH}).submit(BatchWorkspace)"
+                   " [pinned host buffers]")
+        e2e_timing = (f"{pipe_steps} pipelined steps ({PIPE_DEPTH} workspaces, {PIPE_DEPTH} in flight), host wall clock"
+                      " from the first submit to the last wait, max over ranks")
     else:
         e2e_value = e2e_sync_value
         e2e_api = "paper_2408_09662_b200.dist.batch_eval_ranks(tape, BatchWorkspace) [pinned host buffers]"
